@@ -1,0 +1,285 @@
+/*
+ * dedisp_b200.h -- the C-ABI boundary of the B200 dedispersion hot path.
+ *
+ * Plain C types only (no CUDA or torch types in any signature).  Every entry
+ * point returns a dd_status; dd_last_error() gives the thread's last message.
+ * The reference (/root/reference/proj/core, C++20) has no C ABI of its own;
+ * each entry below names the reference function it stands in for, so the
+ * reference's C++ API can be re-implemented over this layer
+ * (include/dedisp/b200.hpp does exactly that; INTEGRATION.md shows the shim
+ * a maintainer would add on the reference side).
+ *
+ * Status mapping (reference error conventions):
+ *   DD_ERR_INVALID_ARGUMENT  <-> std::invalid_argument
+ *                                (kernels.cpp:16-28, :58-81; setup.cpp:31-62)
+ *   DD_ERR_CAPACITY          <-> dedisp::capacity_error (errors.hpp:10-13)
+ *   DD_ERR_CUDA / NO_DEVICE  <-> std::runtime_error (device failure; the
+ *                                reference has no device, so no analogue)
+ *
+ * Layouts (identical to the reference):
+ *   filterbank  float32 [channels][num_samples] channel-major
+ *               (filterbank.hpp:15-26); on the device rows may be padded to
+ *               a pitch (in floats) -- the fast kernels need pitch % 4 == 0.
+ *   shifts      uint32  [num_dms][channels] DM-major (setup.hpp:39-51)
+ *   output      float32 [num_dms][samples_per_second] DM-major
+ *               (kernels.hpp:16-27), optionally with a row pitch.
+ *
+ * Threading: a dd_context belongs to one device and one stream; calls on
+ * one context must be serialised by the caller (one context per thread or a
+ * lock), exactly like the reference's borrowed ThreadPool (kernels.hpp:66-71).
+ */
+#ifndef DEDISP_B200_H
+#define DEDISP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DD_ABI_VERSION 1
+
+typedef enum dd_status {
+  DD_OK = 0,
+  DD_ERR_INVALID_ARGUMENT = 1,
+  DD_ERR_CAPACITY = 2,
+  DD_ERR_CUDA = 3,
+  DD_ERR_NO_DEVICE = 4,
+  DD_ERR_INTERNAL = 5
+} dd_status;
+
+/* ObservationSetup minus its name (setup.hpp:14-33). */
+typedef struct dd_setup {
+  uint32_t samples_per_second;
+  uint32_t channels;
+  double f_min;         /* MHz, centre of channel 0 */
+  double channel_width; /* MHz */
+  double dm_first;      /* pc/cm^3 */
+  double dm_step;       /* pc/cm^3 */
+} dd_setup;
+
+/* Input-staging strategy of a tiled launch (the paper's "local memory or
+ * rely on the cache"). */
+typedef enum dd_staging {
+  DD_STAGING_AUTO = 0,   /* fastest kernel family that supports the config */
+  DD_STAGING_SMEM = 1,   /* per-channel windows staged by TMA bulk copies   */
+  DD_STAGING_DIRECT = 2, /* loads straight from global through L1/L2       */
+  DD_STAGING_REGWIN = 3  /* TMA-staged windows + per-thread register window */
+} dd_staging;
+
+/* KernelConfig (kernels.hpp:40-52) plus the two GPU knobs of the north star:
+ * dm_tile_depth = DM tiles one CTA walks in sequence (0 or 1 = one), and the
+ * staging strategy. */
+typedef struct dd_config {
+  uint32_t items_time;
+  uint32_t items_dm;
+  uint32_t work_time;
+  uint32_t work_dm;
+  uint32_t dm_tile_depth;
+  uint32_t staging; /* dd_staging */
+} dd_config;
+
+/* KernelLimits (kernels.hpp:31-34); {0,0} means the reference defaults
+ * {1024, 256}. */
+typedef struct dd_limits {
+  uint32_t max_block_items;
+  uint32_t max_accumulators;
+} dd_limits;
+
+typedef struct dd_context dd_context;
+typedef struct dd_plan dd_plan;
+
+/* ---------------------------------------------------------------- misc */
+const char* dd_last_error(void);
+int dd_abi_version(void);
+dd_status dd_device_count(int* count);
+
+/* ------------------------------------------------ contexts and streams */
+/* One context per device.  It owns a non-blocking stream unless
+ * dd_context_set_stream() hands it a caller stream (a cudaStream_t passed
+ * as void*).  Replaces the reference's ThreadPool (thread_pool.hpp:15-42). */
+dd_status dd_context_create(int device, dd_context** out);
+dd_status dd_context_destroy(dd_context* ctx);
+dd_status dd_context_set_stream(dd_context* ctx, void* stream);
+void* dd_context_stream(dd_context* ctx);
+dd_status dd_context_synchronize(dd_context* ctx);
+dd_status dd_context_device_info(dd_context* ctx, int* sm_count, int* smem_optin_bytes,
+                                 int* cc_major, int* cc_minor);
+
+/* -------------------------------------------------------------- memory */
+dd_status dd_device_malloc(dd_context* ctx, uint64_t bytes, void** ptr);
+dd_status dd_device_free(dd_context* ctx, void* ptr);
+dd_status dd_host_malloc(uint64_t bytes, void** ptr); /* page-locked */
+dd_status dd_host_free(void* ptr);
+/* Asynchronous on the context stream. */
+dd_status dd_copy_h2d(dd_context* ctx, void* dst, const void* src, uint64_t bytes);
+dd_status dd_copy_d2h(dd_context* ctx, void* dst, const void* src, uint64_t bytes);
+/* Upload a channel-major filterbank into a pitched device buffer
+ * (dst_pitch >= num_samples floats). */
+dd_status dd_upload_filterbank(dd_context* ctx, float* d_dst, uint64_t dst_pitch,
+                               const float* h_src, uint32_t channels, uint64_t num_samples);
+
+/* ---------------------------------------- L0 geometry (setup.cpp) ---- */
+/* ObservationSetup::validate, setup.cpp:31-46 */
+dd_status dd_setup_validate(const dd_setup* setup);
+/* delay_seconds, setup.cpp:48-62 (Eq. 1, FP64, k = 4150) */
+dd_status dd_delay_seconds(double dm, double f_channel_mhz, double f_highest_mhz, double* out);
+/* instance_sizing, setup.cpp:112-137 */
+dd_status dd_instance_sizing(const dd_setup* setup, uint32_t num_dms, uint64_t* num_samples,
+                             uint64_t* flop, uint32_t* max_delay);
+
+/* ---------------------------------------------- K1: shift table ------- */
+/* build_delay_table / build_zero_delay_table (setup.cpp:86-110) computed on
+ * the device in FP64: rows [dm_offset, dm_offset+num_dms) of the full table
+ * are written to d_shifts (uint32 [num_dms][channels]).  max_delay (host
+ * pointer, may be NULL) receives the slice maximum; that read synchronises
+ * the stream.  Used directly by the DM-sharded multi-GPU driver. */
+dd_status dd_delay_table_device(dd_context* ctx, const dd_setup* setup, uint32_t num_dms,
+                                uint32_t dm_offset, int zero, uint32_t* d_shifts,
+                                uint32_t* max_delay);
+/* Host-buffer drop-in for build_delay_table (setup.hpp:75-81): honours the
+ * memory cap (capacity error) and returns the full table in h_shifts. */
+dd_status dd_build_delay_table(dd_context* ctx, const dd_setup* setup, uint32_t num_dms,
+                               uint64_t memory_cap_bytes, int zero, uint32_t* h_shifts,
+                               uint32_t* max_delay);
+
+/* ------------------------------------ L1 configs (kernels.cpp:44-81) -- */
+int dd_config_valid(const dd_config* cfg, uint32_t num_dms, uint32_t samples_per_second,
+                    const dd_limits* limits);
+dd_status dd_validate_config(const dd_config* cfg, uint32_t num_dms,
+                             uint32_t samples_per_second, const dd_limits* limits);
+/* Whether a device kernel family supports cfg for this instance, and which
+ * (resolves DD_STAGING_AUTO).  Returns DD_OK with *family = dd_staging. */
+dd_status dd_config_family(dd_context* ctx, const dd_config* cfg, uint32_t channels,
+                           uint32_t num_dms, uint32_t samples_per_second, uint32_t max_span,
+                           uint32_t* family);
+/* count_loads, count_loads.cpp:9-68 (host arithmetic over a host table). */
+dd_status dd_count_loads(const uint32_t* h_shifts, uint32_t channels, uint32_t num_dms,
+                         uint32_t samples_per_second, const dd_config* cfg, uint64_t* staged,
+                         uint64_t* ideal);
+
+/* -------------------------------------- K2/K3: dedispersion plans ----- */
+/* A plan binds a device shift table and a config to a kernel launch: it
+ * validates (never silently falls back: an explicit staging the config cannot
+ * use is DD_ERR_INVALID_ARGUMENT), runs the per-(DM tile, channel) lo/hi
+ * pre-pass (the min/max scan of kernels.cpp:147-156, done once per table),
+ * sizes shared memory and picks the launch.  cfg == NULL selects the
+ * reference-order kernel (dedisperse_reference_into, kernels.cpp:83-108):
+ * one thread per output.  Creation synchronises the context stream once. */
+dd_status dd_plan_create(dd_context* ctx, const uint32_t* d_shifts, uint32_t channels,
+                         uint32_t num_dms, uint32_t samples_per_second, uint64_t num_samples,
+                         uint64_t in_pitch, const dd_config* cfg, const dd_limits* limits,
+                         dd_plan** out);
+dd_status dd_plan_destroy(dd_plan* plan);
+
+typedef struct dd_plan_info {
+  uint32_t family;        /* dd_staging actually used */
+  uint32_t max_span;      /* max over (DM tile, channel) of hi - lo */
+  uint32_t max_delay;     /* max shift in the table */
+  uint32_t grid_x, grid_y, block_threads;
+  uint32_t smem_bytes;    /* dynamic shared memory per CTA */
+  uint32_t channels_per_stage, stages;
+  uint32_t kernel_launches; /* launches per dd_plan_execute */
+  uint64_t staged_bytes;  /* L2->SMEM bytes per execute (0 for direct) */
+} dd_plan_info;
+dd_status dd_plan_get_info(const dd_plan* plan, dd_plan_info* info);
+
+/* Launch on the context stream, asynchronously: out[dm][j] (row pitch
+ * out_pitch floats, >= samples_per_second) = sum over ch ascending of
+ * in[ch][j + shift[dm][ch]], one fp32 accumulator from 0.0f per output --
+ * bit-identical to dedisperse_reference for every config. */
+dd_status dd_plan_execute(dd_plan* plan, const float* d_in, float* d_out, uint64_t out_pitch);
+
+/* Time `repeats` executions with CUDA events on the context stream after
+ * `warmup` untimed ones (benchmark_config, tuner.cpp:136-170).  seconds[i]
+ * receives each run. */
+dd_status dd_plan_time(dd_plan* plan, const float* d_in, float* d_out, uint64_t out_pitch,
+                       uint32_t warmup, uint32_t repeats, double* seconds);
+
+/* One-shot device-buffer dedispersion: plan + execute + destroy. */
+dd_status dd_dedisperse_device(dd_context* ctx, const float* d_in, uint32_t channels,
+                               uint64_t num_samples, uint64_t in_pitch,
+                               const uint32_t* d_shifts, uint32_t num_dms,
+                               uint32_t samples_per_second, const dd_config* cfg,
+                               const dd_limits* limits, float* d_out);
+
+/* Host-buffer drop-in for dedisperse_reference_into (cfg == NULL,
+ * kernels.cpp:83-108) and dedisperse_tiled_into (kernels.cpp:117-206):
+ * checks the pair (kernels.cpp:16-28), validates cfg against the reference
+ * limits, uploads, runs, downloads h_out (num_dms x samples_per_second).
+ * Synchronous. */
+dd_status dd_dedisperse(dd_context* ctx, const float* h_in, uint32_t channels,
+                        uint64_t num_samples, const uint32_t* h_shifts, uint32_t num_dms,
+                        uint32_t samples_per_second, const dd_config* cfg,
+                        const dd_limits* limits, float* h_out);
+
+/* ---------------------------------------------- synthetic input ------- */
+/* noise_filterbank, filterbank.cpp:60-80: mt19937_64(seed), Box-Muller,
+ * channel-major fill, float(sigma * g).  Host memory; threads = 0 -> all. */
+dd_status dd_noise_filterbank(uint32_t channels, uint64_t num_samples, float sigma,
+                              uint64_t seed, int threads, float* h_out);
+
+/* ------------------------------------------------------- tuner -------- */
+/* enumerate_configs, tuner.cpp:103-134: the reference's divisor space.
+ * Writes min(count, capacity) configs (GPU knobs zeroed). */
+dd_status dd_enumerate_configs(uint32_t num_dms, uint32_t samples_per_second,
+                               const dd_limits* limits, dd_config* out, uint64_t capacity,
+                               uint64_t* count);
+
+typedef struct dd_tune_options {
+  dd_limits limits;
+  uint32_t repeats;       /* timed runs per config (default 10) */
+  uint32_t zero_dm;       /* 1: all-zero table (zero_dm_experiment) */
+  uint64_t seed;          /* noise seed (TuneOptions.seed, default 1) */
+  uint32_t space;         /* 0: GPU space (reference-valid 4-tuples the device
+                             kernels support, x depth x staging);
+                             1: the full reference divisor space */
+  uint32_t max_configs;   /* 0 = no cap */
+} dd_tune_options;
+
+/* The GPU tuning space for an instance (see dd_tune_options.space = 0). */
+dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint32_t num_dms,
+                                   const dd_limits* limits, dd_config* out, uint64_t capacity,
+                                   uint64_t* count);
+
+typedef struct dd_tuning_record {
+  dd_config config;
+  double mean_time;  /* seconds, over the timed repeats */
+  double min_time;
+  double max_time;
+  double gflops;     /* num_dms*s*channels / mean_time / 1e9 */
+  uint32_t timer_warning;
+  uint32_t family;
+} dd_tuning_record;
+
+typedef struct dd_tuning_summary {
+  uint64_t count;
+  uint64_t best_index;     /* select_best, tuner.cpp:172-179 */
+  double mean_gflops;      /* compute_stats, tuner.cpp:181-206 */
+  double stddev_gflops;
+  double snr_optimum;      /* NaN when degenerate */
+  double chebyshev_bound;  /* NaN when degenerate */
+  uint32_t degenerate;
+  uint32_t realtime_pass;
+  double realtime_threshold_gflops; /* analysis.cpp:40-45 */
+  double clock_resolution_s;
+} dd_tuning_summary;
+
+/* tune / zero_dm_experiment (tuner.cpp:43-99, 208-216) on the device:
+ * builds the table on the device, the noise input on the host, then
+ * benchmarks every config of the chosen space sequentially with CUDA events.
+ * records must hold `capacity` entries; summary->count is the space size. */
+dd_status dd_tune(dd_context* ctx, const dd_setup* setup, uint32_t num_dms,
+                  const dd_tune_options* options, dd_tuning_record* records, uint64_t capacity,
+                  dd_tuning_summary* summary);
+
+/* select_best / compute_stats over caller records (pure, replayable). */
+dd_status dd_select_best(const dd_tuning_record* records, uint64_t count, uint64_t* best);
+dd_status dd_compute_stats(const dd_tuning_record* records, uint64_t count, uint64_t best,
+                           dd_tuning_summary* summary);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DEDISP_B200_H */

@@ -1,0 +1,649 @@
+"""Python mirror of the reference's `dedisp` C++ API, over the C-ABI.
+
+Same names, argument meaning and error behaviour as the reference's
+proj/core headers (setup.hpp, filterbank.hpp, kernels.hpp, tuner.hpp,
+analysis.hpp): ``std::invalid_argument`` surfaces as ``ValueError``,
+``capacity_error`` as ``CapacityError``, device failures as ``DeviceError``.
+Host-side value types hold numpy arrays with the reference layouts
+(filterbank float32 [channels][t], table uint32 [d][channels], output
+float32 [d][s]).  Every computation on the hot path runs in the CUDA library;
+nothing here falls back to the CPU.
+
+Device-resident workflows (the bench, the multi-GPU driver) use
+:class:`Context` and :class:`Plan` with raw device pointers (e.g. from
+``torch.Tensor.data_ptr()``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from ._native import CapacityError, DeviceError, check, lib  # noqa: F401
+
+
+# ----------------------------------------------------------------- setup --
+@dataclass(frozen=True)
+class ObservationSetup:
+    """reference setup.hpp:14-33"""
+
+    name: str
+    samples_per_second: int
+    channels: int
+    f_min: float
+    channel_width: float
+    dm_first: float
+    dm_step: float
+
+    def channel_frequency(self, ch: int) -> float:
+        return self.f_min + float(ch) * self.channel_width
+
+    def highest_frequency(self) -> float:
+        return self.channel_frequency(self.channels - 1)
+
+    def trial_dm(self, i: int) -> float:
+        return self.dm_first + float(i) * self.dm_step
+
+    def c(self) -> N.dd_setup:
+        return N.dd_setup(self.samples_per_second, self.channels, self.f_min,
+                          self.channel_width, self.dm_first, self.dm_step)
+
+    def validate(self) -> None:
+        check(lib().dd_setup_validate(C.byref(self.c())))
+
+
+APERTIF = ObservationSetup("Apertif", 20000, 1024, 1420.0, 0.29, 0.0, 0.25)
+LOFAR = ObservationSetup("LOFAR", 200000, 32, 138.0, 0.19, 0.0, 0.25)
+DEFAULT_TABLE_CAP = 1 << 30
+
+
+def builtin_setups() -> List[ObservationSetup]:
+    """reference setup.cpp:139-147"""
+    return [APERTIF, LOFAR]
+
+
+def find_builtin(name: str) -> Optional[ObservationSetup]:
+    for s in builtin_setups():
+        if s.name == name:
+            return s
+    return None
+
+
+@dataclass
+class DelayTable:
+    """reference setup.hpp:39-51 (shifts: uint32 [num_dms][channels])."""
+
+    setup: ObservationSetup
+    num_dms: int
+    shifts: np.ndarray
+    max_delay: int
+
+    def at(self, channel: int, dm: int) -> int:
+        return int(self.shifts[dm, channel])
+
+
+@dataclass
+class ProblemInstance:
+    setup: ObservationSetup
+    num_dms: int
+    num_samples: int
+    flop: int
+    max_delay: int
+
+
+def delay_seconds(dm: float, f_channel_mhz: float, f_highest_mhz: float) -> float:
+    out = C.c_double()
+    check(lib().dd_delay_seconds(dm, f_channel_mhz, f_highest_mhz, C.byref(out)))
+    return out.value
+
+
+def instance_sizing(setup: ObservationSetup, num_dms: int) -> ProblemInstance:
+    t, f, m = C.c_uint64(), C.c_uint64(), C.c_uint32()
+    check(lib().dd_instance_sizing(C.byref(setup.c()), num_dms, C.byref(t), C.byref(f),
+                                   C.byref(m)))
+    return ProblemInstance(setup, num_dms, t.value, f.value, m.value)
+
+
+def _table(setup, num_dms, cap, zero, device):
+    if num_dms < 1:
+        raise ValueError("num_dms must be >= 1")
+    setup.validate()
+    if num_dms * setup.channels * 4 > cap:
+        raise CapacityError(f"delay table of {num_dms * setup.channels * 4} bytes exceeds the "
+                            f"cap of {cap}")
+    sh = np.empty((num_dms, setup.channels), np.uint32)
+    md = C.c_uint32()
+    check(lib().dd_build_delay_table(context(device).handle, C.byref(setup.c()), num_dms, cap,
+                                     int(zero), sh.ctypes.data, C.byref(md)))
+    return DelayTable(setup, num_dms, sh, md.value)
+
+
+def build_delay_table(setup: ObservationSetup, num_dms: int, memory_cap_bytes: int = DEFAULT_TABLE_CAP,
+                      device: int = 0) -> DelayTable:
+    """reference setup.cpp:86-105, computed on the device (K1)."""
+    return _table(setup, num_dms, memory_cap_bytes, False, device)
+
+
+def build_zero_delay_table(setup: ObservationSetup, num_dms: int,
+                           memory_cap_bytes: int = DEFAULT_TABLE_CAP, device: int = 0) -> DelayTable:
+    """reference setup.cpp:107-110"""
+    return _table(setup, num_dms, memory_cap_bytes, True, device)
+
+
+# ------------------------------------------------------------ filterbank --
+@dataclass
+class Filterbank:
+    """reference filterbank.hpp:15-26 (data: float32 [channels][num_samples])."""
+
+    setup: ObservationSetup
+    num_samples: int
+    data: np.ndarray
+
+    def at(self, channel: int, sample: int) -> float:
+        return float(self.data[channel, sample])
+
+
+def noise_filterbank(setup: ObservationSetup, num_samples: int, sigma: float, seed: int,
+                     threads: int = 0) -> Filterbank:
+    """reference filterbank.cpp:60-80 (mt19937_64 + Box-Muller, bit-identical)."""
+    setup.validate()
+    out = np.empty((setup.channels, num_samples), np.float32)
+    check(lib().dd_noise_filterbank(setup.channels, num_samples, sigma, seed, threads,
+                                    out.ctypes.data))
+    return Filterbank(setup, num_samples, out)
+
+
+# --------------------------------------------------------------- kernels --
+@dataclass(frozen=True, order=True)
+class KernelConfig:
+    """reference kernels.hpp:40-52"""
+
+    items_time: int = 1
+    items_dm: int = 1
+    work_time: int = 1
+    work_dm: int = 1
+
+    def tile_time(self) -> int:
+        return self.items_time * self.work_time
+
+    def tile_dm(self) -> int:
+        return self.items_dm * self.work_dm
+
+    def block_items(self) -> int:
+        return self.items_time * self.items_dm
+
+    def accumulators(self) -> int:
+        return self.work_time * self.work_dm
+
+
+@dataclass(frozen=True)
+class KernelLimits:
+    """reference kernels.hpp:31-34"""
+
+    max_block_items: int = 1024
+    max_accumulators: int = 256
+
+    def c(self) -> N.dd_limits:
+        return N.dd_limits(self.max_block_items, self.max_accumulators)
+
+
+@dataclass
+class KernelStats:
+    """reference kernels.hpp:56-64"""
+
+    flop_additions: int = 0
+    staged_loads: int = 0
+
+    def reset(self) -> None:
+        self.flop_additions = 0
+        self.staged_loads = 0
+
+
+@dataclass
+class ExecOptions:
+    """reference kernels.hpp:66-71 plus the GPU knobs (threads is ignored)."""
+
+    threads: int = 0
+    limits: KernelLimits = field(default_factory=KernelLimits)
+    stats: Optional[KernelStats] = None
+    device: int = 0
+    dm_tile_depth: int = 1
+    staging: str = "auto"
+
+
+@dataclass
+class DedispersedSeries:
+    """reference kernels.hpp:16-27 (data: float32 [num_dms][samples_per_second])."""
+
+    num_dms: int = 0
+    samples_per_second: int = 0
+    data: np.ndarray = field(default_factory=lambda: np.empty((0, 0), np.float32))
+
+    def at(self, dm: int, sample: int) -> float:
+        return float(self.data[dm, sample])
+
+
+@dataclass(frozen=True)
+class LoadCounts:
+    staged_loads: int
+    ideal_loads: int
+
+
+def _cfg(cfg: KernelConfig, depth: int = 1, staging: str = "auto") -> N.dd_config:
+    return N.dd_config(cfg.items_time, cfg.items_dm, cfg.work_time, cfg.work_dm, depth,
+                       N.STAGING[staging])
+
+
+def config_valid(cfg: KernelConfig, num_dms: int, samples_per_second: int,
+                 limits: KernelLimits = KernelLimits()) -> bool:
+    return bool(lib().dd_config_valid(C.byref(_cfg(cfg)), num_dms, samples_per_second,
+                                      C.byref(limits.c())))
+
+
+def validate_config(cfg: KernelConfig, num_dms: int, samples_per_second: int,
+                    limits: KernelLimits = KernelLimits()) -> None:
+    check(lib().dd_validate_config(C.byref(_cfg(cfg)), num_dms, samples_per_second,
+                                   C.byref(limits.c())))
+
+
+def _check_pair(fb: Filterbank, table: DelayTable) -> None:
+    """reference kernels.cpp:16-28"""
+    if (fb.setup.channels != table.setup.channels
+            or fb.setup.samples_per_second != table.setup.samples_per_second):
+        raise ValueError("filterbank and delay table describe different setups")
+    if table.num_dms == 0:
+        raise ValueError("delay table holds no trials")
+    need = fb.setup.samples_per_second + table.max_delay
+    if fb.num_samples < need:
+        raise ValueError(f"filterbank too short: need {need} samples per channel, have "
+                         f"{fb.num_samples}")
+
+
+def _run(out: DedispersedSeries, fb: Filterbank, table: DelayTable, cfg, limits, device) -> None:
+    _check_pair(fb, table)
+    d, s = table.num_dms, fb.setup.samples_per_second
+    data = np.ascontiguousarray(fb.data, np.float32)
+    shifts = np.ascontiguousarray(table.shifts, np.uint32)
+    if out.data.shape != (d, s) or out.data.dtype != np.float32 or not out.data.flags.c_contiguous:
+        out.data = np.empty((d, s), np.float32)
+    out.num_dms, out.samples_per_second = d, s
+    check(lib().dd_dedisperse(context(device).handle, data.ctypes.data, fb.setup.channels,
+                              fb.num_samples, shifts.ctypes.data, d, s,
+                              C.byref(cfg) if cfg is not None else None,
+                              C.byref(limits) if limits is not None else None,
+                              out.data.ctypes.data))
+
+
+def dedisperse_reference_into(out: DedispersedSeries, fb: Filterbank, table: DelayTable,
+                              stats: Optional[KernelStats] = None, device: int = 0) -> None:
+    """reference kernels.cpp:83-108, on the device in the same per-output order."""
+    _run(out, fb, table, None, None, device)
+    if stats is not None:
+        total = table.num_dms * fb.setup.samples_per_second * fb.setup.channels
+        stats.flop_additions += total
+        stats.staged_loads += total
+
+
+def dedisperse_reference(fb: Filterbank, table: DelayTable,
+                         stats: Optional[KernelStats] = None, device: int = 0) -> DedispersedSeries:
+    out = DedispersedSeries()
+    dedisperse_reference_into(out, fb, table, stats, device)
+    return out
+
+
+def dedisperse_tiled_into(out: DedispersedSeries, fb: Filterbank, table: DelayTable,
+                          cfg: KernelConfig, options: ExecOptions = ExecOptions()) -> None:
+    """reference kernels.cpp:117-206: bit-identical to dedisperse_reference."""
+    _check_pair(fb, table)
+    validate_config(cfg, table.num_dms, fb.setup.samples_per_second, options.limits)
+    _run(out, fb, table, _cfg(cfg, options.dm_tile_depth, options.staging),
+         options.limits.c(), options.device)
+    if options.stats is not None:
+        options.stats.flop_additions += (table.num_dms * fb.setup.samples_per_second
+                                         * fb.setup.channels)
+        options.stats.staged_loads += count_loads(table, cfg, table.num_dms,
+                                                  fb.setup.samples_per_second).staged_loads
+
+
+def dedisperse_tiled(fb: Filterbank, table: DelayTable, cfg: KernelConfig,
+                     options: ExecOptions = ExecOptions()) -> DedispersedSeries:
+    out = DedispersedSeries()
+    dedisperse_tiled_into(out, fb, table, cfg, options)
+    return out
+
+
+def count_loads(table: DelayTable, cfg: KernelConfig, num_dms: int,
+                samples_per_second: int) -> LoadCounts:
+    """reference count_loads.cpp:9-68"""
+    if num_dms == 0 or num_dms != table.num_dms:
+        raise ValueError("delay table does not cover the requested trial count")
+    sh = np.ascontiguousarray(table.shifts, np.uint32)
+    st, idl = C.c_uint64(), C.c_uint64()
+    check(lib().dd_count_loads(sh.ctypes.data, table.setup.channels, num_dms, samples_per_second,
+                               C.byref(_cfg(cfg)), C.byref(st), C.byref(idl)))
+    return LoadCounts(st.value, idl.value)
+
+
+# ------------------------------------------------- device-side objects ---
+class Context:
+    """One dd_context: a device and a stream (replaces the reference ThreadPool)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib().dd_context_create(device, C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def close(self) -> None:
+        if self.handle:
+            lib().dd_context_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def set_stream(self, stream_ptr: int) -> None:
+        check(lib().dd_context_set_stream(self.handle, C.c_void_p(stream_ptr or None)))
+
+    def synchronize(self) -> None:
+        check(lib().dd_context_synchronize(self.handle))
+
+    def info(self):
+        sm, smem, ma, mi = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        check(lib().dd_context_device_info(self.handle, C.byref(sm), C.byref(smem), C.byref(ma),
+                                           C.byref(mi)))
+        return {"sm_count": sm.value, "smem_optin": smem.value, "cc": (ma.value, mi.value)}
+
+    def delay_table(self, setup: ObservationSetup, num_dms: int, d_shifts: int,
+                    dm_offset: int = 0, zero: bool = False) -> int:
+        """K1 into a device buffer (rows dm_offset..); returns the slice max."""
+        md = C.c_uint32()
+        check(lib().dd_delay_table_device(self.handle, C.byref(setup.c()), num_dms, dm_offset,
+                                          int(zero), C.c_void_p(d_shifts), C.byref(md)))
+        return md.value
+
+    def plan(self, d_shifts: int, channels: int, num_dms: int, samples_per_second: int,
+             num_samples: int, in_pitch: int, cfg: Optional[KernelConfig] = None,
+             dm_tile_depth: int = 1, staging: str = "auto",
+             limits: KernelLimits = KernelLimits()) -> "Plan":
+        return Plan(self, d_shifts, channels, num_dms, samples_per_second, num_samples, in_pitch,
+                    cfg, dm_tile_depth, staging, limits)
+
+
+class Plan:
+    """dd_plan: a table + config bound to one kernel launch."""
+
+    def __init__(self, ctx: Context, d_shifts, channels, num_dms, s, num_samples, in_pitch,
+                 cfg, depth, staging, limits):
+        self.ctx = ctx
+        self.num_dms, self.s, self.channels = num_dms, s, channels
+        h = C.c_void_p()
+        kc = _cfg(cfg, depth, staging) if cfg is not None else None
+        check(lib().dd_plan_create(ctx.handle, C.c_void_p(d_shifts), channels, num_dms, s,
+                                   num_samples, in_pitch, C.byref(kc) if kc is not None else None,
+                                   C.byref(limits.c()), C.byref(h)))
+        self.handle = h
+
+    def close(self) -> None:
+        if self.handle:
+            lib().dd_plan_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        i = N.dd_plan_info()
+        check(lib().dd_plan_get_info(self.handle, C.byref(i)))
+        d = {f: getattr(i, f) for f, _ in N.dd_plan_info._fields_}
+        d["family"] = N.STAGING_NAME.get(d["family"], d["family"])
+        return d
+
+    def execute(self, d_in: int, d_out: int, out_pitch: Optional[int] = None) -> None:
+        check(lib().dd_plan_execute(self.handle, C.c_void_p(d_in), C.c_void_p(d_out),
+                                    out_pitch or self.s))
+
+    def time(self, d_in: int, d_out: int, warmup: int = 1, repeats: int = 10,
+             out_pitch: Optional[int] = None) -> List[float]:
+        runs = (C.c_double * max(repeats, 1))()
+        check(lib().dd_plan_time(self.handle, C.c_void_p(d_in), C.c_void_p(d_out),
+                                 out_pitch or self.s, warmup, repeats, runs))
+        return list(runs[:repeats])
+
+
+_contexts = {}
+
+
+def context(device: int = 0) -> Context:
+    if device not in _contexts:
+        _contexts[device] = Context(device)
+    return _contexts[device]
+
+
+def device_count() -> int:
+    n = C.c_int()
+    st = lib().dd_device_count(C.byref(n))
+    return n.value if st == N.DD_OK else 0
+
+
+# ----------------------------------------------------------------- tuner --
+@dataclass
+class TuningRecord:
+    """reference tuner.hpp:17-23 plus the GPU knobs."""
+
+    config: KernelConfig
+    runs: List[float] = field(default_factory=list)
+    mean_time: float = 0.0
+    gflops: float = 0.0
+    timer_warning: bool = False
+    dm_tile_depth: int = 1
+    staging: str = "auto"
+    family: str = ""
+
+    def c(self) -> N.dd_tuning_record:
+        r = N.dd_tuning_record()
+        r.config = _cfg(self.config, self.dm_tile_depth, self.staging)
+        r.mean_time = self.mean_time
+        r.gflops = self.gflops
+        return r
+
+
+@dataclass
+class TuningStats:
+    mean_gflops: float = 0.0
+    stddev_gflops: float = 0.0
+    snr_optimum: Optional[float] = None
+    chebyshev_bound: Optional[float] = None
+    degenerate: bool = False
+
+
+@dataclass
+class TuningResult:
+    """reference tuner.hpp:37-55"""
+
+    setup: ObservationSetup
+    num_dms: int
+    zero_dm: bool
+    limits: KernelLimits
+    repeats: int
+    seed: int
+    records: List[TuningRecord]
+    best_index: int
+    stats: TuningStats
+    realtime_threshold_gflops: float
+    realtime_pass: bool
+    rng_id: str = "mt19937_64/box-muller"
+    clock_resolution_s: float = 0.5e-6
+
+    def best(self) -> TuningRecord:
+        return self.records[self.best_index]
+
+
+def enumerate_configs(num_dms: int, samples_per_second: int,
+                      limits: KernelLimits = KernelLimits()) -> List[KernelConfig]:
+    """reference tuner.cpp:103-134"""
+    n = C.c_uint64()
+    check(lib().dd_enumerate_configs(num_dms, samples_per_second, C.byref(limits.c()), None, 0,
+                                     C.byref(n)))
+    buf = (N.dd_config * max(n.value, 1))()
+    check(lib().dd_enumerate_configs(num_dms, samples_per_second, C.byref(limits.c()), buf,
+                                     n.value, C.byref(n)))
+    return [KernelConfig(b.items_time, b.items_dm, b.work_time, b.work_dm) for b in buf[:n.value]]
+
+
+def enumerate_gpu_configs(setup: ObservationSetup, num_dms: int,
+                          limits: KernelLimits = KernelLimits(), device: int = 0):
+    """The GPU tuning space: [(KernelConfig, dm_tile_depth, staging)]."""
+    ctx = context(device)
+    n = C.c_uint64()
+    check(lib().dd_enumerate_gpu_configs(ctx.handle, C.byref(setup.c()), num_dms,
+                                         C.byref(limits.c()), None, 0, C.byref(n)))
+    buf = (N.dd_config * max(n.value, 1))()
+    check(lib().dd_enumerate_gpu_configs(ctx.handle, C.byref(setup.c()), num_dms,
+                                         C.byref(limits.c()), buf, n.value, C.byref(n)))
+    return [(KernelConfig(b.items_time, b.items_dm, b.work_time, b.work_dm), b.dm_tile_depth,
+             N.STAGING_NAME[b.staging]) for b in buf[:n.value]]
+
+
+def select_best(records: Sequence[TuningRecord]) -> int:
+    """reference tuner.cpp:172-179 (ties: fewer block items, then config order)."""
+    if not records:
+        raise ValueError("no records to select from")
+    arr = (N.dd_tuning_record * len(records))(*[r.c() for r in records])
+    b = C.c_uint64()
+    check(lib().dd_select_best(arr, len(records), C.byref(b)))
+    return b.value
+
+
+def compute_stats(records: Sequence[TuningRecord], best_index: int) -> TuningStats:
+    """reference tuner.cpp:181-206"""
+    if not records:
+        raise ValueError("no records to summarize")
+    arr = (N.dd_tuning_record * len(records))(*[r.c() for r in records])
+    s = N.dd_tuning_summary()
+    check(lib().dd_compute_stats(arr, len(records), best_index, C.byref(s)))
+    return _stats(s)
+
+
+def _stats(s) -> TuningStats:
+    deg = bool(s.degenerate)
+    return TuningStats(s.mean_gflops, s.stddev_gflops, None if deg else s.snr_optimum,
+                       None if deg else s.chebyshev_bound, deg)
+
+
+def _sweep(setup, num_dms, limits, repeats, seed, zero, full_space, max_configs, device):
+    ctx = context(device)
+    opt = N.dd_tune_options(limits.c(), repeats, int(zero), seed, int(full_space), max_configs)
+    n = C.c_uint64()
+    if full_space:
+        check(lib().dd_enumerate_configs(num_dms, setup.samples_per_second, C.byref(limits.c()),
+                                         None, 0, C.byref(n)))
+    else:
+        check(lib().dd_enumerate_gpu_configs(ctx.handle, C.byref(setup.c()), num_dms,
+                                             C.byref(limits.c()), None, 0, C.byref(n)))
+    recs = (N.dd_tuning_record * max(n.value, 1))()
+    summ = N.dd_tuning_summary()
+    check(lib().dd_tune(ctx.handle, C.byref(setup.c()), num_dms, C.byref(opt), recs, n.value,
+                        C.byref(summ)))
+    out = []
+    for r in recs[:summ.count]:
+        k = r.config
+        out.append(TuningRecord(KernelConfig(k.items_time, k.items_dm, k.work_time, k.work_dm),
+                                [], r.mean_time, r.gflops, bool(r.timer_warning),
+                                k.dm_tile_depth, N.STAGING_NAME[k.staging],
+                                N.STAGING_NAME.get(r.family, "")))
+    return TuningResult(setup, num_dms, zero, limits, repeats, seed, out, summ.best_index,
+                        _stats(summ), summ.realtime_threshold_gflops, bool(summ.realtime_pass))
+
+
+def tune(setup: ObservationSetup, num_dms: int, limits: KernelLimits = KernelLimits(),
+         repeats: int = 10, seed: int = 1, full_reference_space: bool = False,
+         max_configs: int = 0, device: int = 0) -> TuningResult:
+    """reference tuner.cpp:208-211 on the device (CUDA-event timing)."""
+    return _sweep(setup, num_dms, limits, repeats, seed, False, full_reference_space,
+                  max_configs, device)
+
+
+def zero_dm_experiment(setup: ObservationSetup, num_dms: int, limits: KernelLimits = KernelLimits(),
+                       repeats: int = 10, seed: int = 1, full_reference_space: bool = False,
+                       max_configs: int = 0, device: int = 0) -> TuningResult:
+    """reference tuner.cpp:213-216"""
+    return _sweep(setup, num_dms, limits, repeats, seed, True, full_reference_space,
+                  max_configs, device)
+
+
+@dataclass
+class FixedConfigReport:
+    config: tuple
+    total_gflops: float
+    fixed_gflops: List[float]
+    speedup_over_fixed: List[float]
+
+
+def best_fixed_config(results: Sequence[TuningResult]) -> FixedConfigReport:
+    """reference tuner.cpp:218-261 (identity = 4-tuple + GPU knobs)."""
+    if not results:
+        raise ValueError("no tuning results given")
+    first = results[0].setup
+    for r in results:
+        if (r.setup.name != first.name or r.setup.samples_per_second != first.samples_per_second
+                or r.setup.channels != first.channels):
+            raise ValueError("tuning results mix different setups")
+        if not r.records:
+            raise ValueError("a tuning result holds no records")
+    by = {}
+    for i, r in enumerate(results):
+        for rec in r.records:
+            key = (rec.config, rec.dm_tile_depth, rec.staging)
+            v = by.setdefault(key, [])
+            if len(v) == i:
+                v.append(rec.gflops)
+    best = None
+    for key in sorted(by, key=lambda k: (k[0], k[1], k[2])):
+        v = by[key]
+        if len(v) != len(results):
+            continue
+        tot = sum(v)
+        if best is None or tot > best[1]:
+            best = (key, tot, v)
+    if best is None:
+        raise ValueError("no configuration is valid in every instance")
+    key, tot, v = best
+    return FixedConfigReport(key, tot, list(v),
+                             [r.best().gflops / g for r, g in zip(results, v)])
+
+
+def default_instances() -> List[int]:
+    """reference tuner.cpp:292-296"""
+    return [2 ** k for k in range(1, 13)]
+
+
+# -------------------------------------------------- analysis (metric defs) --
+def realtime_threshold_gflops(setup: ObservationSetup, num_dms: int) -> float:
+    """reference analysis.cpp:40-45"""
+    setup.validate()
+    if num_dms == 0:
+        raise ValueError("need at least one trial DM")
+    return num_dms * setup.samples_per_second * setup.channels / 1e9
+
+
+def ai_bounds(num_dms: int, samples_per_second: int, channels: int):
+    """reference analysis.cpp:11-21 -> (no_reuse, reuse_bound) flop/byte."""
+    if not (num_dms and samples_per_second and channels):
+        raise ValueError("instance dimensions must all be positive")
+    return 0.25, 1.0 / (4.0 * (1.0 / num_dms + 1.0 / samples_per_second + 1.0 / channels))
+
+
+def algorithmic_bytes(num_dms: int, samples_per_second: int, channels: int) -> int:
+    """Eq. 2 no-reuse traffic 4*(d*s*c + d*s + d*c)."""
+    d, s, c = num_dms, samples_per_second, channels
+    return 4 * (d * s * c + d * s + d * c)
+
+
+def roofline_gflops(num_dms: int, samples_per_second: int, channels: int, hbm_gbs: float) -> float:
+    d, s, c = num_dms, samples_per_second, channels
+    return d * s * c / (algorithmic_bytes(d, s, c) / (hbm_gbs * 1e9)) / 1e9

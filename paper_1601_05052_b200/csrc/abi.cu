@@ -1,0 +1,756 @@
+// abi.cu -- implementation of the C-ABI in include/dedisp_b200.h:
+// contexts, memory, the reference's geometry and config rules, device shift
+// tables, dedispersion plans and the host-buffer drop-in entry points.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+
+namespace ddb {
+
+static thread_local std::string g_error;
+
+dd_status fail(dd_status st, const std::string& msg) {
+  g_error = msg;
+  return st;
+}
+
+dd_status cuda_fail(cudaError_t e, const char* where) {
+  g_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ? DD_ERR_NO_DEVICE
+                                                                     : DD_ERR_CUDA;
+}
+
+void clear_error() { g_error.clear(); }
+
+dd_limits effective_limits(const dd_limits* l) {
+  dd_limits out{1024u, 256u};  // KernelLimits defaults, kernels.hpp:31-34
+  if (l != nullptr && (l->max_block_items != 0 || l->max_accumulators != 0)) out = *l;
+  return out;
+}
+
+// ObservationSetup::validate, reference setup.cpp:31-46.
+bool setup_ok(const dd_setup* s, std::string* why) {
+  auto bad = [&](const char* m) {
+    if (why) *why = m;
+    return false;
+  };
+  if (s == nullptr) return bad("setup is null");
+  if (s->samples_per_second < 1) return bad("samples_per_second must be >= 1");
+  if (s->channels < 1) return bad("channels must be >= 1");
+  if (!(s->f_min > 0.0) || !std::isfinite(s->f_min))
+    return bad("f_min must be positive and finite");
+  if (!(s->channel_width > 0.0) || !std::isfinite(s->channel_width))
+    return bad("channel_width must be positive and finite");
+  if (!(s->dm_step > 0.0) || !std::isfinite(s->dm_step))
+    return bad("dm_step must be positive and finite");
+  if (!(s->dm_first >= 0.0) || !std::isfinite(s->dm_first))
+    return bad("dm_first must be non-negative and finite");
+  return true;
+}
+
+// setup.hpp:23-29
+double channel_frequency(const dd_setup& s, uint32_t ch) {
+  return s.f_min + static_cast<double>(ch) * s.channel_width;
+}
+double trial_dm(const dd_setup& s, uint32_t i) {
+  return s.dm_first + static_cast<double>(i) * s.dm_step;
+}
+
+}  // namespace ddb
+
+using namespace ddb;
+
+#define DD_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+#define DD_TRY(call)                     \
+  do {                                   \
+    dd_status s_ = (call);               \
+    if (s_ != DD_OK) return s_;          \
+  } while (0)
+
+extern "C" {
+
+const char* dd_last_error(void) { return g_error.c_str(); }
+int dd_abi_version(void) { return DD_ABI_VERSION; }
+
+dd_status dd_device_count(int* count) {
+  if (count == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "count is null");
+  *count = 0;
+  const cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  return DD_OK;
+}
+
+// ------------------------------------------------------------ contexts --
+dd_status dd_context_create(int device, dd_context** out) {
+  if (out == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "out is null");
+  *out = nullptr;
+  int n = 0;
+  DD_TRY(dd_device_count(&n));
+  if (device < 0 || device >= n)
+    return fail(DD_ERR_NO_DEVICE, "device " + std::to_string(device) + " not present");
+  DD_CUDA(cudaSetDevice(device));
+  auto* c = new dd_context;
+  c->device = device;
+  cudaDeviceProp p{};
+  cudaError_t e = cudaGetDeviceProperties(&p, device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_scratch, 16);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev_start);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev_stop);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "dd_context_create");
+  }
+  c->own_stream = true;
+  c->sm_count = p.multiProcessorCount;
+  c->smem_optin = static_cast<int>(p.sharedMemPerBlockOptin);
+  c->cc_major = p.major;
+  c->cc_minor = p.minor;
+  if (p.major < 10)
+    return delete c, fail(DD_ERR_NO_DEVICE, "device is not sm_100 class (compute capability " +
+                                                std::to_string(p.major) + "." +
+                                                std::to_string(p.minor) + ")");
+  *out = c;
+  return DD_OK;
+}
+
+dd_status dd_context_destroy(dd_context* c) {
+  if (c == nullptr) return DD_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  cudaFree(c->d_scratch);
+  cudaEventDestroy(c->ev_start);
+  cudaEventDestroy(c->ev_stop);
+  delete c;
+  return DD_OK;
+}
+
+dd_status dd_context_set_stream(dd_context* c, void* stream) {
+  if (c == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "context is null");
+  DD_CUDA(cudaSetDevice(c->device));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  if (stream == nullptr) {
+    DD_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  } else {
+    c->stream = static_cast<cudaStream_t>(stream);
+    c->own_stream = false;
+  }
+  return DD_OK;
+}
+
+void* dd_context_stream(dd_context* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+dd_status dd_context_synchronize(dd_context* c) {
+  if (c == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "context is null");
+  DD_CUDA(cudaSetDevice(c->device));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  return DD_OK;
+}
+
+dd_status dd_context_device_info(dd_context* c, int* sm_count, int* smem_optin, int* cc_major,
+                                 int* cc_minor) {
+  if (c == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "context is null");
+  if (sm_count) *sm_count = c->sm_count;
+  if (smem_optin) *smem_optin = c->smem_optin;
+  if (cc_major) *cc_major = c->cc_major;
+  if (cc_minor) *cc_minor = c->cc_minor;
+  return DD_OK;
+}
+
+// -------------------------------------------------------------- memory --
+dd_status dd_device_malloc(dd_context* c, uint64_t bytes, void** ptr) {
+  if (c == nullptr || ptr == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  DD_CUDA(cudaSetDevice(c->device));
+  const cudaError_t e = cudaMalloc(ptr, bytes ? bytes : 16);
+  if (e == cudaErrorMemoryAllocation)
+    return fail(DD_ERR_CAPACITY, "device allocation of " + std::to_string(bytes) + " bytes failed");
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  return DD_OK;
+}
+
+dd_status dd_device_free(dd_context* c, void* ptr) {
+  if (c == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "context is null");
+  DD_CUDA(cudaSetDevice(c->device));
+  DD_CUDA(cudaFree(ptr));
+  return DD_OK;
+}
+
+dd_status dd_host_malloc(uint64_t bytes, void** ptr) {
+  if (ptr == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "ptr is null");
+  const cudaError_t e = cudaMallocHost(ptr, bytes ? bytes : 16);
+  if (e == cudaErrorMemoryAllocation)
+    return fail(DD_ERR_CAPACITY, "pinned allocation of " + std::to_string(bytes) + " bytes failed");
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
+  return DD_OK;
+}
+
+dd_status dd_host_free(void* ptr) {
+  DD_CUDA(cudaFreeHost(ptr));
+  return DD_OK;
+}
+
+dd_status dd_copy_h2d(dd_context* c, void* dst, const void* src, uint64_t bytes) {
+  if (c == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "context is null");
+  DD_CUDA(cudaSetDevice(c->device));
+  DD_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+  return DD_OK;
+}
+
+dd_status dd_copy_d2h(dd_context* c, void* dst, const void* src, uint64_t bytes) {
+  if (c == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "context is null");
+  DD_CUDA(cudaSetDevice(c->device));
+  DD_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+  return DD_OK;
+}
+
+dd_status dd_upload_filterbank(dd_context* c, float* d_dst, uint64_t dst_pitch,
+                               const float* h_src, uint32_t channels, uint64_t num_samples) {
+  if (c == nullptr || d_dst == nullptr || h_src == nullptr)
+    return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  if (dst_pitch < num_samples) return fail(DD_ERR_INVALID_ARGUMENT, "pitch below num_samples");
+  DD_CUDA(cudaSetDevice(c->device));
+  DD_CUDA(cudaMemcpy2DAsync(d_dst, dst_pitch * 4, h_src, num_samples * 4, num_samples * 4,
+                            channels, cudaMemcpyHostToDevice, c->stream));
+  return DD_OK;
+}
+
+// ------------------------------------------------------------ geometry --
+dd_status dd_setup_validate(const dd_setup* s) {
+  std::string why;
+  if (!setup_ok(s, &why)) return fail(DD_ERR_INVALID_ARGUMENT, why);
+  return DD_OK;
+}
+
+// delay_seconds, reference setup.cpp:48-62.
+dd_status dd_delay_seconds(double dm, double f_ch, double f_hi, double* out) {
+  if (out == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "out is null");
+  if (!std::isfinite(dm) || !std::isfinite(f_ch) || !std::isfinite(f_hi))
+    return fail(DD_ERR_INVALID_ARGUMENT, "delay_seconds: non-finite input");
+  if (dm < 0.0) return fail(DD_ERR_INVALID_ARGUMENT, "delay_seconds: dm must be non-negative");
+  if (f_ch <= 0.0 || f_hi <= 0.0)
+    return fail(DD_ERR_INVALID_ARGUMENT, "delay_seconds: frequencies must be positive");
+  if (f_ch > f_hi)
+    return fail(DD_ERR_INVALID_ARGUMENT,
+                "delay_seconds: channel frequency above the reference frequency");
+  const double inv_low = 1.0 / (f_ch * f_ch);
+  const double inv_high = 1.0 / (f_hi * f_hi);
+  *out = 4150.0 * dm * (inv_low - inv_high);
+  return DD_OK;
+}
+
+// instance_sizing, reference setup.cpp:112-137.
+dd_status dd_instance_sizing(const dd_setup* s, uint32_t num_dms, uint64_t* num_samples,
+                             uint64_t* flop, uint32_t* max_delay) {
+  DD_TRY(dd_setup_validate(s));
+  if (num_dms < 1) return fail(DD_ERR_INVALID_ARGUMENT, "num_dms must be >= 1");
+  double worst = 0.0;
+  DD_TRY(dd_delay_seconds(trial_dm(*s, num_dms - 1), channel_frequency(*s, 0),
+                          channel_frequency(*s, s->channels - 1), &worst));
+  const double worst_samples = worst * static_cast<double>(s->samples_per_second);
+  if (worst_samples >= 4294967295.0)
+    return fail(DD_ERR_CAPACITY, "maximum shift does not fit 32 bits");
+  const uint32_t md = static_cast<uint32_t>(std::llround(worst_samples));
+  const uint64_t rate = s->samples_per_second;
+  const uint64_t blocks = (rate + md + rate - 1) / rate;
+  unsigned __int128 t = static_cast<unsigned __int128>(blocks) * rate;
+  unsigned __int128 f = static_cast<unsigned __int128>(num_dms) * rate * s->channels;
+  if (t > std::numeric_limits<uint64_t>::max() || f > std::numeric_limits<uint64_t>::max())
+    return fail(DD_ERR_CAPACITY, "sizing overflow");
+  if (num_samples) *num_samples = static_cast<uint64_t>(t);
+  if (flop) *flop = static_cast<uint64_t>(f);
+  if (max_delay) *max_delay = md;
+  return DD_OK;
+}
+
+// --------------------------------------------------------- K1: tables --
+dd_status dd_delay_table_device(dd_context* c, const dd_setup* s, uint32_t num_dms,
+                                uint32_t dm_offset, int zero, uint32_t* d_shifts,
+                                uint32_t* max_delay) {
+  if (c == nullptr || d_shifts == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  DD_TRY(dd_setup_validate(s));
+  if (num_dms < 1) return fail(DD_ERR_INVALID_ARGUMENT, "num_dms must be >= 1");
+  // delay_seconds rejects a non-finite trial DM (setup.cpp:49-51).
+  if (!std::isfinite(trial_dm(*s, dm_offset + num_dms - 1)))
+    return fail(DD_ERR_INVALID_ARGUMENT, "delay_seconds: non-finite input");
+  DD_CUDA(cudaSetDevice(c->device));
+  const uint64_t entries = static_cast<uint64_t>(num_dms) * s->channels;
+  if (zero) {
+    DD_CUDA(cudaMemsetAsync(d_shifts, 0, entries * 4, c->stream));
+    if (max_delay) *max_delay = 0;
+    return DD_OK;
+  }
+  DD_CUDA(cudaMemsetAsync(c->d_scratch, 0, 4, c->stream));
+  DD_CUDA(launch_delay_table(d_shifts, c->d_scratch, num_dms, s->channels, dm_offset, s->f_min,
+                             s->channel_width, s->dm_first, s->dm_step,
+                             static_cast<double>(s->samples_per_second), c->stream));
+  if (max_delay) {
+    DD_CUDA(cudaMemcpyAsync(max_delay, c->d_scratch, 4, cudaMemcpyDeviceToHost, c->stream));
+    DD_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  return DD_OK;
+}
+
+// build_delay_table / build_zero_delay_table (setup.cpp:66-110) with the
+// table computed by K1 and returned in host memory.
+dd_status dd_build_delay_table(dd_context* c, const dd_setup* s, uint32_t num_dms,
+                               uint64_t cap, int zero, uint32_t* h_shifts, uint32_t* max_delay) {
+  if (c == nullptr || h_shifts == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  DD_TRY(dd_setup_validate(s));
+  if (num_dms < 1) return fail(DD_ERR_INVALID_ARGUMENT, "num_dms must be >= 1");
+  const unsigned __int128 bytes = static_cast<unsigned __int128>(num_dms) * s->channels * 4u;
+  if (bytes > cap)
+    return fail(DD_ERR_CAPACITY, "delay table of " + std::to_string(static_cast<uint64_t>(bytes)) +
+                                     " bytes exceeds the cap of " + std::to_string(cap));
+  void* d = nullptr;
+  DD_TRY(dd_device_malloc(c, static_cast<uint64_t>(bytes), &d));
+  uint32_t md = 0;
+  dd_status st = dd_delay_table_device(c, s, num_dms, 0, zero, static_cast<uint32_t*>(d), &md);
+  if (st == DD_OK) {
+    const cudaError_t e = cudaMemcpyAsync(h_shifts, d, static_cast<size_t>(bytes),
+                                          cudaMemcpyDeviceToHost, c->stream);
+    const cudaError_t e2 = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) st = cuda_fail(e, "table download");
+    else if (e2 != cudaSuccess) st = cuda_fail(e2, "table download");
+  }
+  cudaFree(d);
+  if (st == DD_OK && max_delay) *max_delay = md;
+  return st;
+}
+
+// ------------------------------------------------------------- configs --
+// config_valid / validate_config, reference kernels.cpp:44-81.
+int dd_config_valid(const dd_config* k, uint32_t num_dms, uint32_t s, const dd_limits* limits) {
+  if (k == nullptr) return 0;
+  const dd_limits L = effective_limits(limits);
+  if (!k->items_time || !k->items_dm || !k->work_time || !k->work_dm) return 0;
+  const uint64_t tt = static_cast<uint64_t>(k->items_time) * k->work_time;
+  const uint64_t td = static_cast<uint64_t>(k->items_dm) * k->work_dm;
+  if (tt > s || s % tt != 0) return 0;
+  if (td > num_dms || num_dms % td != 0) return 0;
+  if (static_cast<uint64_t>(k->items_time) * k->items_dm > L.max_block_items) return 0;
+  if (static_cast<uint64_t>(k->work_time) * k->work_dm > L.max_accumulators) return 0;
+  return 1;
+}
+
+dd_status dd_validate_config(const dd_config* k, uint32_t num_dms, uint32_t s,
+                             const dd_limits* limits) {
+  if (k == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "config is null");
+  const dd_limits L = effective_limits(limits);
+  if (!k->items_time || !k->items_dm || !k->work_time || !k->work_dm)
+    return fail(DD_ERR_INVALID_ARGUMENT, "kernel config parameters must all be positive");
+  const uint64_t tt = static_cast<uint64_t>(k->items_time) * k->work_time;
+  const uint64_t td = static_cast<uint64_t>(k->items_dm) * k->work_dm;
+  if (tt > s || s % tt != 0)
+    return fail(DD_ERR_INVALID_ARGUMENT, "items_time * work_time = " + std::to_string(tt) +
+                                             " does not divide s = " + std::to_string(s));
+  if (td > num_dms || num_dms % td != 0)
+    return fail(DD_ERR_INVALID_ARGUMENT, "items_dm * work_dm = " + std::to_string(td) +
+                                             " does not divide the trial count " +
+                                             std::to_string(num_dms));
+  if (static_cast<uint64_t>(k->items_time) * k->items_dm > L.max_block_items)
+    return fail(DD_ERR_INVALID_ARGUMENT, "items_time * items_dm exceeds the block limit of " +
+                                             std::to_string(L.max_block_items));
+  if (static_cast<uint64_t>(k->work_time) * k->work_dm > L.max_accumulators)
+    return fail(DD_ERR_INVALID_ARGUMENT, "work_time * work_dm exceeds the accumulator limit of " +
+                                             std::to_string(L.max_accumulators));
+  if (k->staging > DD_STAGING_REGWIN) return fail(DD_ERR_INVALID_ARGUMENT, "unknown staging mode");
+  return DD_OK;
+}
+
+// count_loads, reference count_loads.cpp:9-68.
+dd_status dd_count_loads(const uint32_t* sh, uint32_t channels, uint32_t num_dms, uint32_t s,
+                         const dd_config* k, uint64_t* staged, uint64_t* ideal) {
+  if (sh == nullptr || k == nullptr || channels == 0)
+    return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  if (num_dms == 0) return fail(DD_ERR_INVALID_ARGUMENT, "delay table does not cover the requested trial count");
+  if (!k->items_time || !k->items_dm || !k->work_time || !k->work_dm)
+    return fail(DD_ERR_INVALID_ARGUMENT, "kernel config parameters must all be positive");
+  const uint64_t tt = static_cast<uint64_t>(k->items_time) * k->work_time;
+  const uint64_t td = static_cast<uint64_t>(k->items_dm) * k->work_dm;
+  if (tt > s || s % tt != 0 || td > num_dms || num_dms % td != 0)
+    return fail(DD_ERR_INVALID_ARGUMENT, "kernel config does not tile this instance");
+  uint64_t st = 0, id = 0;
+  const uint64_t tiles_time = s / tt;
+  for (uint64_t dm0 = 0; dm0 < num_dms; dm0 += td)
+    for (uint32_t ch = 0; ch < channels; ++ch) {
+      uint32_t lo = sh[dm0 * channels + ch], hi = lo;
+      for (uint64_t l = 1; l < td; ++l) {
+        const uint32_t v = sh[(dm0 + l) * channels + ch];
+        lo = std::min(lo, v);
+        hi = std::max(hi, v);
+      }
+      st += (static_cast<uint64_t>(hi - lo) + tt) * tiles_time;
+    }
+  std::vector<uint32_t> col(num_dms);
+  for (uint32_t ch = 0; ch < channels; ++ch) {
+    for (uint32_t dm = 0; dm < num_dms; ++dm) col[dm] = sh[static_cast<uint64_t>(dm) * channels + ch];
+    std::sort(col.begin(), col.end());
+    uint64_t begin = col[0], end = static_cast<uint64_t>(col[0]) + s;
+    for (uint32_t dm = 1; dm < num_dms; ++dm) {
+      if (col[dm] > end) {
+        id += end - begin;
+        begin = col[dm];
+      }
+      end = static_cast<uint64_t>(col[dm]) + s;
+    }
+    id += end - begin;
+  }
+  if (staged) *staged = st;
+  if (ideal) *ideal = id;
+  return DD_OK;
+}
+
+// -------------------------------------------------------------- plans --
+namespace {
+
+constexpr uint32_t kSmemBudget = 112 * 1024;  // aim for 2 CTAs per SM
+
+// Staged-family geometry for a config: shared-memory slots, stage count.
+bool smem_geometry(const dd_context* c, uint32_t tile_time, uint32_t tile_dm, uint32_t channels,
+                   uint32_t max_span, uint32_t* win_cap, uint32_t* rec_bytes, uint32_t* cps,
+                   uint32_t* nstage, uint32_t* smem) {
+  const uint64_t wc = (static_cast<uint64_t>(max_span) + tile_time + 6u + 3u) & ~3ull;
+  const uint64_t rb = ddb::plan_rec_bytes(tile_dm);
+  const uint64_t slot = rb + 4 * wc;
+  const uint64_t limit = static_cast<uint64_t>(c->smem_optin);
+  // Prefer 3 stages of several channels within the 2-CTA budget; degrade
+  // to fewer channels, then to 2 stages, then to the opt-in maximum.
+  const uint32_t cps_opts[] = {8, 4, 2, 1};
+  for (uint64_t budget : {static_cast<uint64_t>(kSmemBudget), limit}) {
+    for (uint32_t ns : {3u, 2u}) {
+      for (uint32_t cp : cps_opts) {
+        if (cp > channels && cp != 1) continue;
+        const uint64_t bytes = 128 + static_cast<uint64_t>(ns) * cp * slot;
+        if (bytes <= budget && bytes <= limit) {
+          *win_cap = static_cast<uint32_t>(wc);
+          *rec_bytes = static_cast<uint32_t>(rb);
+          *cps = cp;
+          *nstage = ns;
+          *smem = static_cast<uint32_t>(bytes);
+          return true;
+        }
+      }
+    }
+  }
+  return false;
+}
+
+dd_status max_of_device_table(dd_context* c, const uint32_t* d_shifts, uint64_t n, uint32_t* out) {
+  DD_CUDA(cudaMemsetAsync(c->d_scratch, 0, 4, c->stream));
+  DD_CUDA(launch_max_u32(d_shifts, n, c->d_scratch, c->stream));
+  DD_CUDA(cudaMemcpyAsync(out, c->d_scratch, 4, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  return DD_OK;
+}
+
+}  // namespace
+
+dd_status dd_config_family(dd_context* c, const dd_config* k, uint32_t channels,
+                           uint32_t num_dms, uint32_t s, uint32_t max_span, uint32_t* family) {
+  if (c == nullptr || k == nullptr || family == nullptr)
+    return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  const uint64_t block = static_cast<uint64_t>(k->items_time) * k->items_dm;
+  const uint32_t tile_time = k->items_time * k->work_time;
+  const uint32_t tile_dm = k->items_dm * k->work_dm;
+  (void)num_dms;
+  (void)s;
+  bool smem_ok = smem_variant_ok(k->work_dm, k->work_time, block);
+  if (smem_ok) {
+    uint32_t a, b, cc, d, e;
+    smem_ok = smem_geometry(c, tile_time, tile_dm, channels, max_span, &a, &b, &cc, &d, &e);
+  }
+  switch (k->staging) {
+    case DD_STAGING_AUTO:
+      *family = smem_ok ? DD_STAGING_SMEM : DD_STAGING_DIRECT;
+      return DD_OK;
+    case DD_STAGING_SMEM:
+      if (!smem_ok)
+        return fail(DD_ERR_INVALID_ARGUMENT,
+                    "staging=smem: no staged kernel for this config (work_dm x work_time "
+                    "variant, block size or shared-memory window)");
+      *family = DD_STAGING_SMEM;
+      return DD_OK;
+    case DD_STAGING_DIRECT:
+      *family = DD_STAGING_DIRECT;
+      return DD_OK;
+    default:
+      return fail(DD_ERR_INVALID_ARGUMENT, "staging mode not available in this build");
+  }
+}
+
+dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t channels,
+                         uint32_t num_dms, uint32_t s, uint64_t num_samples, uint64_t in_pitch,
+                         const dd_config* k, const dd_limits* limits, dd_plan** out) {
+  if (out == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "out is null");
+  *out = nullptr;
+  if (c == nullptr || d_shifts == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  if (channels == 0 || s == 0) return fail(DD_ERR_INVALID_ARGUMENT, "empty setup");
+  if (num_dms == 0) return fail(DD_ERR_INVALID_ARGUMENT, "delay table holds no trials");
+  if (in_pitch < num_samples) return fail(DD_ERR_INVALID_ARGUMENT, "input pitch below num_samples");
+  if (k != nullptr) DD_TRY(dd_validate_config(k, num_dms, s, limits));
+  DD_CUDA(cudaSetDevice(c->device));
+
+  uint32_t md = 0;
+  DD_TRY(max_of_device_table(c, d_shifts, static_cast<uint64_t>(num_dms) * channels, &md));
+  // check_pair, reference kernels.cpp:22-27
+  const uint64_t needed = static_cast<uint64_t>(s) + md;
+  if (num_samples < needed)
+    return fail(DD_ERR_INVALID_ARGUMENT, "filterbank too short: need " + std::to_string(needed) +
+                                             " samples per channel, have " +
+                                             std::to_string(num_samples));
+
+  auto* p = new dd_plan;
+  p->ctx = c;
+  p->d_shifts = d_shifts;
+  p->max_delay = md;
+  ddb::TiledArgs& a = p->args;
+  a.in_pitch = in_pitch;
+  a.shifts = d_shifts;
+  a.channels = channels;
+  a.s = s;
+  a.num_dms = num_dms;
+
+  if (k == nullptr) {
+    p->reference_order = true;
+    p->family = DD_STAGING_DIRECT;
+    *out = p;
+    return DD_OK;
+  }
+
+  a.items_time = k->items_time;
+  a.items_dm = k->items_dm;
+  a.work_time = k->work_time;
+  a.work_dm = k->work_dm;
+  a.tile_time = k->items_time * k->work_time;
+  a.tile_dm = k->items_dm * k->work_dm;
+  a.tiles_time = s / a.tile_time;
+  a.tiles_dm = num_dms / a.tile_dm;
+  a.depth = std::max<uint32_t>(1, k->dm_tile_depth);
+  a.depth = std::min(a.depth, a.tiles_dm);
+
+  const uint64_t block = static_cast<uint64_t>(k->items_time) * k->items_dm;
+  const bool want_smem = k->staging == DD_STAGING_AUTO || k->staging == DD_STAGING_SMEM;
+  const bool smem_possible = want_smem && in_pitch % 4 == 0 &&
+                             smem_variant_ok(k->work_dm, k->work_time, block);
+  if (k->staging == DD_STAGING_REGWIN) {
+    delete p;
+    return fail(DD_ERR_INVALID_ARGUMENT, "staging mode not available in this build");
+  }
+
+  if (smem_possible) {
+    a.rec_bytes = ddb::plan_rec_bytes(a.tile_dm);
+    const uint64_t rec_total = static_cast<uint64_t>(a.tiles_dm) * channels * a.rec_bytes;
+    cudaError_t e = cudaMalloc(&p->d_rec, rec_total);
+    uint32_t scratch[4] = {0, 0, 0, 0};
+    unsigned long long* d_sum = reinterpret_cast<unsigned long long*>(c->d_scratch + 2);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->d_scratch, 0, 16, c->stream);
+    if (e == cudaSuccess)
+      e = launch_plan(d_shifts, p->d_rec, c->d_scratch, d_sum, channels, a.tiles_dm, a.tile_dm,
+                      a.rec_bytes, c->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(scratch, c->d_scratch, 16, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    p->max_span = scratch[0];
+    uint64_t span_sum = 0;
+    std::memcpy(&span_sum, scratch + 2, 8);
+    if (e != cudaSuccess) {
+      cudaFree(p->d_rec);
+      delete p;
+      return cuda_fail(e, "plan pre-pass");
+    }
+    uint32_t win_cap = 0, rec_bytes = 0, cps = 0, nstage = 0, smem = 0;
+    if (smem_geometry(c, a.tile_time, a.tile_dm, channels, p->max_span, &win_cap, &rec_bytes,
+                      &cps, &nstage, &smem)) {
+      a.win_cap = win_cap;
+      a.cps = cps;
+      a.nstage = nstage;
+      a.rec = p->d_rec;
+      p->smem_fn = find_smem_kernel(k->work_dm, k->work_time);
+      p->smem = smem;
+      p->threads = static_cast<uint32_t>(block);
+      const uint64_t groups_dm = (a.tiles_dm + a.depth - 1) / a.depth;
+      p->blocks = static_cast<uint32_t>(groups_dm * a.tiles_time);
+      p->family = DD_STAGING_SMEM;
+      e = prepare_smem(p->smem_fn, smem);
+      if (e != cudaSuccess) {
+        cudaFree(p->d_rec);
+        delete p;
+        return cuda_fail(e, "cudaFuncSetAttribute");
+      }
+      // count_loads' staged elements (count_loads.cpp:33-45) x 4 bytes.
+      p->staged_bytes = 4ull * a.tiles_time *
+                        (span_sum + static_cast<uint64_t>(a.tiles_dm) * channels * a.tile_time);
+      *out = p;
+      return DD_OK;
+    }
+    cudaFree(p->d_rec);
+    p->d_rec = nullptr;
+  }
+  if (k->staging == DD_STAGING_SMEM) {
+    delete p;
+    return fail(DD_ERR_INVALID_ARGUMENT,
+                "staging=smem: no staged kernel for this config (work_dm x work_time variant, "
+                "block size, input pitch or shared-memory window)");
+  }
+  // Direct family: pack small tiles, virtualise oversize blocks.
+  const uint32_t bi = static_cast<uint32_t>(std::min<uint64_t>(block, 0xffffffffull));
+  a.pack = bi >= 256 ? 1 : 256 / bi;
+  a.vthreads = a.pack * bi;
+  p->threads = std::min<uint32_t>(256, (a.vthreads + 31) & ~31u);
+  const uint64_t tiles = static_cast<uint64_t>(a.tiles_time) * a.tiles_dm;
+  const uint64_t blocks = (tiles + a.pack - 1) / a.pack;
+  if (blocks > 0x7fffffffULL) {
+    delete p;
+    return fail(DD_ERR_CAPACITY, "too many tiles for one launch");
+  }
+  p->blocks = static_cast<uint32_t>(blocks);
+  p->family = DD_STAGING_DIRECT;
+  *out = p;
+  return DD_OK;
+}
+
+dd_status dd_plan_destroy(dd_plan* p) {
+  if (p == nullptr) return DD_OK;
+  if (p->d_rec) {
+    cudaSetDevice(p->ctx->device);
+    cudaFree(p->d_rec);
+  }
+  delete p;
+  return DD_OK;
+}
+
+dd_status dd_plan_get_info(const dd_plan* p, dd_plan_info* info) {
+  if (p == nullptr || info == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  std::memset(info, 0, sizeof(*info));
+  info->family = p->family;
+  info->max_span = p->max_span;
+  info->max_delay = p->max_delay;
+  info->grid_x = p->blocks;
+  info->grid_y = 1;
+  info->block_threads = p->threads;
+  info->smem_bytes = p->smem;
+  info->channels_per_stage = p->args.cps;
+  info->stages = p->args.nstage;
+  info->kernel_launches = 1;
+  info->staged_bytes = p->staged_bytes;
+  if (p->reference_order) {
+    const uint64_t n = static_cast<uint64_t>(p->args.num_dms) * p->args.s;
+    info->grid_x = static_cast<uint32_t>((n + 255) / 256);
+    info->block_threads = 256;
+  }
+  return DD_OK;
+}
+
+dd_status dd_plan_execute(dd_plan* p, const float* d_in, float* d_out, uint64_t out_pitch) {
+  if (p == nullptr || d_in == nullptr || d_out == nullptr)
+    return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  if (out_pitch < p->args.s) return fail(DD_ERR_INVALID_ARGUMENT, "output pitch below s");
+  dd_context* c = p->ctx;
+  DD_CUDA(cudaSetDevice(c->device));
+  if (p->reference_order) {
+    DD_CUDA(launch_reference(d_in, p->args.in_pitch, p->d_shifts, d_out, out_pitch,
+                             p->args.channels, p->args.s, p->args.num_dms, c->stream));
+    return DD_OK;
+  }
+  ddb::TiledArgs a = p->args;
+  a.in = d_in;
+  a.out = d_out;
+  a.out_pitch = out_pitch;
+  if (p->family == DD_STAGING_SMEM) {
+    if ((reinterpret_cast<uintptr_t>(d_in) & 15u) != 0)
+      return fail(DD_ERR_INVALID_ARGUMENT, "staged kernels need a 16-byte aligned input");
+    DD_CUDA(launch_smem(p->smem_fn, a, p->blocks, p->threads, p->smem, c->stream));
+  } else {
+    DD_CUDA(launch_direct(a, p->blocks, p->threads, c->stream));
+  }
+  return DD_OK;
+}
+
+dd_status dd_plan_time(dd_plan* p, const float* d_in, float* d_out, uint64_t out_pitch,
+                       uint32_t warmup, uint32_t repeats, double* seconds) {
+  if (p == nullptr || (repeats > 0 && seconds == nullptr))
+    return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  dd_context* c = p->ctx;
+  for (uint32_t i = 0; i < warmup; ++i) DD_TRY(dd_plan_execute(p, d_in, d_out, out_pitch));
+  for (uint32_t i = 0; i < repeats; ++i) {
+    DD_CUDA(cudaEventRecord(c->ev_start, c->stream));
+    DD_TRY(dd_plan_execute(p, d_in, d_out, out_pitch));
+    DD_CUDA(cudaEventRecord(c->ev_stop, c->stream));
+    DD_CUDA(cudaEventSynchronize(c->ev_stop));
+    float ms = 0.0f;
+    DD_CUDA(cudaEventElapsedTime(&ms, c->ev_start, c->ev_stop));
+    seconds[i] = static_cast<double>(ms) * 1e-3;
+  }
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  return DD_OK;
+}
+
+dd_status dd_dedisperse_device(dd_context* c, const float* d_in, uint32_t channels,
+                               uint64_t num_samples, uint64_t in_pitch, const uint32_t* d_shifts,
+                               uint32_t num_dms, uint32_t s, const dd_config* k,
+                               const dd_limits* limits, float* d_out) {
+  dd_plan* p = nullptr;
+  DD_TRY(dd_plan_create(c, d_shifts, channels, num_dms, s, num_samples, in_pitch, k, limits, &p));
+  dd_status st = dd_plan_execute(p, d_in, d_out, s);
+  dd_plan_destroy(p);
+  return st;
+}
+
+// Host-buffer drop-in for dedisperse_reference_into / dedisperse_tiled_into.
+dd_status dd_dedisperse(dd_context* c, const float* h_in, uint32_t channels, uint64_t num_samples,
+                        const uint32_t* h_shifts, uint32_t num_dms, uint32_t s,
+                        const dd_config* k, const dd_limits* limits, float* h_out) {
+  if (c == nullptr || h_in == nullptr || h_shifts == nullptr || h_out == nullptr)
+    return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  if (num_dms == 0) return fail(DD_ERR_INVALID_ARGUMENT, "delay table holds no trials");
+  if (channels == 0 || s == 0) return fail(DD_ERR_INVALID_ARGUMENT, "empty setup");
+  const uint64_t entries = static_cast<uint64_t>(num_dms) * channels;
+  uint32_t md = 0;
+  for (uint64_t i = 0; i < entries; ++i) md = std::max(md, h_shifts[i]);
+  const uint64_t needed = static_cast<uint64_t>(s) + md;
+  if (num_samples < needed)
+    return fail(DD_ERR_INVALID_ARGUMENT, "filterbank too short: need " + std::to_string(needed) +
+                                             " samples per channel, have " +
+                                             std::to_string(num_samples));
+  if (k != nullptr) DD_TRY(dd_validate_config(k, num_dms, s, limits));
+  DD_CUDA(cudaSetDevice(c->device));
+  const uint64_t pitch = (num_samples + 3) & ~3ull;
+  void *d_in = nullptr, *d_sh = nullptr, *d_out = nullptr;
+  dd_status st = dd_device_malloc(c, pitch * channels * 4, &d_in);
+  if (st == DD_OK) st = dd_device_malloc(c, entries * 4, &d_sh);
+  if (st == DD_OK) st = dd_device_malloc(c, static_cast<uint64_t>(num_dms) * s * 4, &d_out);
+  if (st == DD_OK)
+    st = dd_upload_filterbank(c, static_cast<float*>(d_in), pitch, h_in, channels, num_samples);
+  if (st == DD_OK) st = dd_copy_h2d(c, d_sh, h_shifts, entries * 4);
+  if (st == DD_OK)
+    st = dd_dedisperse_device(c, static_cast<float*>(d_in), channels, num_samples, pitch,
+                              static_cast<uint32_t*>(d_sh), num_dms, s, k, limits,
+                              static_cast<float*>(d_out));
+  if (st == DD_OK) st = dd_copy_d2h(c, h_out, d_out, static_cast<uint64_t>(num_dms) * s * 4);
+  if (st == DD_OK) {
+    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) st = cuda_fail(e, "dd_dedisperse");
+  }
+  cudaFree(d_in);
+  cudaFree(d_sh);
+  cudaFree(d_out);
+  return st;
+}
+
+}  // extern "C"

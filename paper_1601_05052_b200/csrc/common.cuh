@@ -1,0 +1,110 @@
+// common.cuh -- shared device helpers and launch descriptors for the
+// sm_100a dedispersion kernels.  Inline PTX only (no CUTLASS/CuTe needed:
+// the hot path uses 1-D bulk copies, not tensor maps).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ddb {
+
+// ----------------------------------------------------------------- PTX --
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+
+// Make mbarrier initialisation visible to the async (TMA) proxy.
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// 1-D TMA bulk copy global -> shared, completion counted on `bar` in bytes.
+// dst/src 16-byte aligned, bytes a multiple of 16 (SASS: UBLKCP.S.G).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+// Two IEEE round-to-nearest fp32 adds in one instruction (SASS: FADD2).
+// Each lane is an independent correctly-rounded add, so the per-output
+// accumulation order (and hence bit-exactness) is unchanged.
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rr;\n\t"
+      "mov.b64 ra, {%2, %3};\n\t"
+      "mov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rr, ra, rb;\n\t"
+      "mov.b64 {%0, %1}, rr;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+
+// ------------------------------------------------------------ launches --
+// Per-(DM tile, channel) plan record, produced by k_plan (table.cu) and
+// staged into shared memory next to the channel's window:
+//   u32 lo, u32 span (= hi - lo), u32 pad[2], u32 off[tile_dm] (= shift - lo)
+// padded to a multiple of 16 bytes.  The min/max scan is the reference's
+// kernels.cpp:147-156, done once per (table, tile_dm) instead of per tile.
+struct PlanRec {
+  uint32_t lo;
+  uint32_t span;
+  uint32_t pad0, pad1;
+};
+
+__host__ __device__ inline uint32_t plan_rec_bytes(uint32_t tile_dm) {
+  return ((16u + 4u * tile_dm) + 15u) & ~15u;
+}
+
+struct TiledArgs {
+  const float* in;
+  uint64_t in_pitch;  // floats, multiple of 4 for the staged families
+  const uint8_t* rec; // [tiles_dm][channels] records, rec_bytes each
+  const uint32_t* shifts;  // DM-major table (direct family)
+  float* out;
+  uint64_t out_pitch;  // floats
+  uint32_t channels, s, num_dms;
+  uint32_t items_time, items_dm, work_time, work_dm;
+  uint32_t tile_time, tile_dm, tiles_time, tiles_dm;
+  uint32_t depth;      // DM tiles per CTA
+  uint32_t win_cap;    // floats per staged channel window (multiple of 4)
+  uint32_t rec_bytes;
+  uint32_t cps;        // channels per pipeline stage
+  uint32_t nstage;
+  uint32_t pack;       // tiles per CTA (direct family)
+  uint32_t vthreads;   // virtual threads per CTA (direct family)
+};
+
+}  // namespace ddb

@@ -1,0 +1,78 @@
+// internal.hpp -- shared between the C-ABI translation units (not installed).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/dedisp_b200.h"
+#include "common.cuh"
+
+struct dd_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sm_count = 0;
+  int smem_optin = 0;
+  int cc_major = 0, cc_minor = 0;
+  uint32_t* d_scratch = nullptr;  // 4 x u32 reduction slots
+  cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+};
+
+struct dd_plan {
+  dd_context* ctx = nullptr;
+  uint32_t family = DD_STAGING_DIRECT;
+  bool reference_order = false;
+  ddb::TiledArgs args{};
+  const uint32_t* d_shifts = nullptr;
+  uint8_t* d_rec = nullptr;
+  void (*smem_fn)(const ddb::TiledArgs) = nullptr;
+  uint32_t blocks = 0, threads = 0, smem = 0;
+  uint32_t grid_y = 1;
+  uint32_t max_span = 0, max_delay = 0;
+  uint64_t staged_bytes = 0;
+};
+
+namespace ddb {
+
+// error state (abi.cu)
+dd_status fail(dd_status st, const std::string& msg);
+dd_status cuda_fail(cudaError_t e, const char* where);
+void clear_error();
+
+// launchers (table.cu, dedisp.cu)
+cudaError_t launch_delay_table(uint32_t* d_shifts, uint32_t* d_max, uint32_t num_dms,
+                               uint32_t channels, uint32_t dm_offset, double f_min, double width,
+                               double dm_first, double dm_step, double rate, cudaStream_t st);
+cudaError_t launch_plan(const uint32_t* d_shifts, uint8_t* d_rec, uint32_t* d_max_span,
+                        unsigned long long* d_span_sum, uint32_t channels, uint32_t tiles_dm, uint32_t tile_dm,
+                        uint32_t rec_bytes, cudaStream_t st);
+cudaError_t launch_max_u32(const uint32_t* d_v, uint64_t n, uint32_t* d_out, cudaStream_t st);
+
+using KernelFn = void (*)(const TiledArgs);
+// Staged-kernel variant for work_dm x work_time; nullptr when not
+// instantiated.  *max_threads = the variant's block-size cap.
+KernelFn find_smem_kernel(uint32_t k, uint32_t w, uint32_t* max_threads = nullptr);
+// True when the staged family can run cfg (block size within the variant's cap).
+inline bool smem_variant_ok(uint32_t k, uint32_t w, uint64_t block) {
+  uint32_t cap = 0;
+  return find_smem_kernel(k, w, &cap) != nullptr && block <= cap;
+}
+cudaError_t launch_reference(const float* in, uint64_t pitch, const uint32_t* shifts, float* out,
+                             uint64_t out_pitch, uint32_t channels, uint32_t s, uint32_t num_dms,
+                             cudaStream_t st);
+cudaError_t launch_direct(const TiledArgs& a, uint32_t blocks, uint32_t threads,
+                          cudaStream_t st);
+cudaError_t launch_smem(KernelFn fn, const TiledArgs& a, uint32_t blocks, uint32_t threads,
+                        uint32_t smem, cudaStream_t st);
+cudaError_t prepare_smem(KernelFn fn, uint32_t smem);
+
+// host logic shared with the tuner (abi.cu)
+dd_limits effective_limits(const dd_limits* l);
+bool setup_ok(const dd_setup* s, std::string* why);
+double channel_frequency(const dd_setup& s, uint32_t ch);
+double trial_dm(const dd_setup& s, uint32_t i);
+
+}  // namespace ddb

@@ -1,0 +1,123 @@
+// table.cu -- K1: the FP64 shift table on the device, and the per-(DM tile,
+// channel) plan pre-pass consumed by the staged kernels.
+//
+// K1 restates build_delay_table (reference setup.cpp:86-105) with every
+// FP64 operation spelled as an explicitly rounded intrinsic, so nvcc cannot
+// contract a*b+c into an FMA: the device then evaluates exactly the host's
+// sequence  f = f_min + ch*width;  DM = dm_first + i*dm_step;
+//           sec = (4150*DM) * (1/(f*f) - 1/(f_hi*f_hi));  llround(sec*s)
+// and reproduces the reference table bit-for-bit (tests/test_gpu_table.py).
+// An FP32 evaluation would flip thousands of entries.
+#include "common.cuh"
+
+namespace ddb {
+
+__device__ __forceinline__ double channel_freq(double f_min, double width, uint32_t ch) {
+  return __dadd_rn(f_min, __dmul_rn(static_cast<double>(ch), width));
+}
+
+__global__ void k_delay_table(uint32_t* __restrict__ shifts, uint32_t* __restrict__ max_out,
+                              uint32_t num_dms, uint32_t channels, uint32_t dm_offset,
+                              double f_min, double width, double dm_first, double dm_step,
+                              double rate) {
+  const uint64_t n = static_cast<uint64_t>(num_dms) * channels;
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint32_t v = 0;
+  if (i < n) {
+    const uint32_t dm = static_cast<uint32_t>(i / channels);
+    const uint32_t ch = static_cast<uint32_t>(i - static_cast<uint64_t>(dm) * channels);
+    const double f_hi = channel_freq(f_min, width, channels - 1);
+    const double f = channel_freq(f_min, width, ch);
+    const double trial =
+        __dadd_rn(dm_first, __dmul_rn(static_cast<double>(dm + dm_offset), dm_step));
+    const double inv_low = __ddiv_rn(1.0, __dmul_rn(f, f));
+    const double inv_high = __ddiv_rn(1.0, __dmul_rn(f_hi, f_hi));
+    const double sec = __dmul_rn(__dmul_rn(4150.0, trial), __dsub_rn(inv_low, inv_high));
+    v = static_cast<uint32_t>(llround(__dmul_rn(sec, rate)));  // half away from zero
+    shifts[i] = v;
+  }
+  v = __reduce_max_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0 && max_out != nullptr) atomicMax(max_out, v);
+}
+
+// Plan pre-pass: one thread per (DM tile b, channel ch).  Scans the tile's
+// shifts with no ordering assumed (the reference's kernels.cpp:147-156 and
+// count_loads.cpp:36-42 make the same choice), writes the record and folds
+// the span into a global maximum used to size shared memory.
+__global__ void k_plan(const uint32_t* __restrict__ shifts, uint8_t* __restrict__ rec,
+                       uint32_t* __restrict__ max_span, unsigned long long* __restrict__ span_sum,
+                       uint32_t channels, uint32_t tiles_dm, uint32_t tile_dm,
+                       uint32_t rec_bytes) {
+  const uint64_t n = static_cast<uint64_t>(tiles_dm) * channels;
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint32_t span = 0;
+  if (i < n) {
+    const uint32_t b = static_cast<uint32_t>(i / channels);
+    const uint32_t ch = static_cast<uint32_t>(i - static_cast<uint64_t>(b) * channels);
+    const uint32_t* col = shifts + static_cast<uint64_t>(b) * tile_dm * channels + ch;
+    uint32_t lo = col[0], hi = lo;
+    for (uint32_t l = 1; l < tile_dm; ++l) {
+      const uint32_t v = col[static_cast<uint64_t>(l) * channels];
+      lo = min(lo, v);
+      hi = max(hi, v);
+    }
+    span = hi - lo;
+    uint32_t* r = reinterpret_cast<uint32_t*>(rec + i * rec_bytes);
+    r[0] = lo;
+    r[1] = span;
+    r[2] = 0;
+    r[3] = 0;
+    for (uint32_t l = 0; l < tile_dm; ++l) r[4 + l] = col[static_cast<uint64_t>(l) * channels] - lo;
+  }
+  const uint32_t sum = __reduce_add_sync(0xffffffffu, span);
+  span = __reduce_max_sync(0xffffffffu, span);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(max_span, span);
+    atomicAdd(span_sum, static_cast<unsigned long long>(sum));
+  }
+}
+
+// Maximum over a uint32 array (max_delay of a caller-supplied device table,
+// needed for the reference's check_pair, kernels.cpp:22-27).
+__global__ void k_max_u32(const uint32_t* __restrict__ v, uint64_t n, uint32_t* __restrict__ out) {
+  uint32_t m = 0;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    m = max(m, v[i]);
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+cudaError_t launch_max_u32(const uint32_t* d_v, uint64_t n, uint32_t* d_out, cudaStream_t st) {
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  if (blocks == 0) blocks = 1;
+  k_max_u32<<<static_cast<uint32_t>(blocks), 256, 0, st>>>(d_v, n, d_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_delay_table(uint32_t* d_shifts, uint32_t* d_max, uint32_t num_dms,
+                               uint32_t channels, uint32_t dm_offset, double f_min, double width,
+                               double dm_first, double dm_step, double rate, cudaStream_t st) {
+  const uint64_t n = static_cast<uint64_t>(num_dms) * channels;
+  const uint32_t threads = 256;
+  const uint64_t blocks = (n + threads - 1) / threads;
+  if (blocks > 0x7fffffffULL) return cudaErrorInvalidValue;
+  k_delay_table<<<static_cast<uint32_t>(blocks), threads, 0, st>>>(
+      d_shifts, d_max, num_dms, channels, dm_offset, f_min, width, dm_first, dm_step, rate);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plan(const uint32_t* d_shifts, uint8_t* d_rec, uint32_t* d_max_span,
+                        unsigned long long* d_span_sum, uint32_t channels, uint32_t tiles_dm, uint32_t tile_dm,
+                        uint32_t rec_bytes, cudaStream_t st) {
+  const uint64_t n = static_cast<uint64_t>(tiles_dm) * channels;
+  const uint32_t threads = 128;
+  const uint64_t blocks = (n + threads - 1) / threads;
+  k_plan<<<static_cast<uint32_t>(blocks), threads, 0, st>>>(d_shifts, d_rec, d_max_span,
+                                                            d_span_sum, channels, tiles_dm, tile_dm,
+                                                            rec_bytes);
+  return cudaGetLastError();
+}
+
+}  // namespace ddb

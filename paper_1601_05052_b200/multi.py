@@ -1,0 +1,118 @@
+"""DM-sharded multi-GPU driver (BASELINE config 4).
+
+One process per GPU (torchrun), torch.distributed/NCCL for the plumbing.
+Every DM row is independent and costs s*c additions, so rank r of N owns the
+contiguous DM range shard_range(d, N, r): its shift-table slice is built on
+its own device by K1 (dm_offset = first row, no table traffic at all), the
+full input block arrives once (H2D on rank 0, then ONE broadcast -- the
+path's only exchange, C1), and the rank writes its output rows in place.
+Outputs stay resident (the paper's pipeline assumption) or are
+gathered to rank 0 (C2) on request.  Because shards are disjoint rows, the
+N-rank output equals the 1-rank output bit for bit.
+
+The plumbing functions (shard_range, broadcast_input, gather_rows) take
+plain torch tensors so they are exercised on CPU with the gloo backend
+(tests/test_multi.py); the compute goes only through the CUDA library.
+"""
+from __future__ import annotations
+
+import os
+from typing import List, Optional, Tuple
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import api
+
+
+def world() -> Tuple[int, int]:
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def shard_range(num_dms: int, world_size: int, rank: int, align: int = 1) -> Tuple[int, int]:
+    """Contiguous DM range (offset, count) of `rank`.  Units of `align` rows
+    (the config's tile_dm) are dealt out as evenly as possible, earlier ranks
+    taking the remainder, so every shard stays tileable."""
+    if world_size < 1 or not 0 <= rank < world_size:
+        raise ValueError("bad rank/world size")
+    if align < 1 or num_dms % align != 0:
+        raise ValueError(f"tile_dm {align} does not divide the trial count {num_dms}")
+    units = num_dms // align
+    base, extra = divmod(units, world_size)
+    start = rank * base + min(rank, extra)
+    count = base + (1 if rank < extra else 0)
+    return start * align, count * align
+
+
+def broadcast_input(block: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:
+    """C1: the filterbank block from `src` to every rank (NCCL over NVLink on
+    the GPU box, gloo on CPU in tests)."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.broadcast(block, src=src, group=group)
+    return block
+
+
+def gather_rows(local: torch.Tensor, num_dms: int, align: int = 1, dst: int = 0,
+                group=None) -> Optional[torch.Tensor]:
+    """C2: assemble the DM-major output on `dst` from every rank's rows.
+    Shards may differ in size, so ranks send padded blocks and `dst` trims."""
+    rank, n = world()
+    if n == 1:
+        return local
+    counts = [shard_range(num_dms, n, r, align)[1] for r in range(n)]
+    width = local.shape[1]
+    pad = torch.zeros((max(counts), width), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    bufs = [torch.empty_like(pad) for _ in range(n)] if rank == dst else None
+    dist.gather(pad, bufs, dst=dst, group=group)
+    if rank != dst:
+        return None
+    return torch.cat([b[:c] for b, c in zip(bufs, counts)], dim=0)
+
+
+class ShardedDedisperser:
+    """This rank's share of one dedispersion instance on its GPU."""
+
+    def __init__(self, setup: api.ObservationSetup, num_dms: int, cfg: api.KernelConfig,
+                 dm_tile_depth: int = 1, staging: str = "auto", device: Optional[int] = None):
+        self.rank, self.world = world()
+        self.setup, self.num_dms, self.cfg = setup, num_dms, cfg
+        self.device = torch.cuda.current_device() if device is None else device
+        torch.cuda.set_device(self.device)
+        self.offset, self.count = shard_range(num_dms, self.world, self.rank, cfg.tile_dm())
+        inst = api.instance_sizing(setup, num_dms)
+        self.num_samples = inst.num_samples
+        self.pitch = (self.num_samples + 3) // 4 * 4
+        c, s = setup.channels, setup.samples_per_second
+        self.ctx = api.context(self.device)
+        self.stream = torch.cuda.current_stream(self.device)
+        self.ctx.set_stream(self.stream.cuda_stream)  # one stream with torch/NCCL ordering
+        self.shifts = torch.empty((self.count, c), dtype=torch.int32, device=self.device)
+        self.max_delay = self.ctx.delay_table(setup, self.count, self.shifts.data_ptr(),
+                                              dm_offset=self.offset)
+        self.block = torch.empty((c, self.pitch), dtype=torch.float32, device=self.device)
+        self.out = torch.empty((self.count, s), dtype=torch.float32, device=self.device)
+        self.plan = self.ctx.plan(self.shifts.data_ptr(), c, self.count, s, self.num_samples,
+                                  self.pitch, cfg, dm_tile_depth, staging)
+
+    @property
+    def flop(self) -> int:
+        """Additions this rank performs per pass."""
+        return self.count * self.setup.samples_per_second * self.setup.channels
+
+    def load(self, host_block: Optional[torch.Tensor]) -> None:
+        """H2D on rank 0 (pinned host tensor [c][t]), then broadcast (C1)."""
+        if self.rank == 0:
+            assert host_block is not None
+            self.block[:, : self.num_samples].copy_(host_block, non_blocking=True)
+        broadcast_input(self.block, src=0)
+
+    def run(self) -> torch.Tensor:
+        self.plan.execute(self.block.data_ptr(), self.out.data_ptr())
+        return self.out
+
+    def gather(self) -> Optional[torch.Tensor]:
+        return gather_rows(self.out, self.num_dms, self.cfg.tile_dm())
