@@ -232,7 +232,8 @@ def run_ours(args):
     cfg = api.KernelConfig(*cfgt[:4])
     dd = multi.ShardedDedisperser(setup, d, cfg, cfgt[4], cfgt[5], device=local)
     c, s, t = setup.channels, setup.samples_per_second, dd.num_samples
-    stream = torch.cuda.current_stream()
+    stream = dd.stream
+    torch.cuda.set_stream(stream)  # events, flushes and copies share the library's stream
 
     host = None
     if rank == 0:

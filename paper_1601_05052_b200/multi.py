@@ -88,8 +88,10 @@ class ShardedDedisperser:
         self.pitch = (self.num_samples + 3) // 4 * 4
         c, s = setup.channels, setup.samples_per_second
         self.ctx = api.context(self.device)
-        self.stream = torch.cuda.current_stream(self.device)
-        self.ctx.set_stream(self.stream.cuda_stream)  # one stream with torch/NCCL ordering
+        # one dedicated stream shared by the library, torch copies and NCCL;
+        # callers run under `with torch.cuda.stream(dd.stream)`
+        self.stream = torch.cuda.Stream(self.device)
+        self.ctx.set_stream(self.stream.cuda_stream)
         self.shifts = torch.empty((self.count, c), dtype=torch.int32, device=self.device)
         self.max_delay = self.ctx.delay_table(setup, self.count, self.shifts.data_ptr(),
                                               dm_offset=self.offset)
@@ -105,14 +107,17 @@ class ShardedDedisperser:
 
     def load(self, host_block: Optional[torch.Tensor]) -> None:
         """H2D on rank 0 (pinned host tensor [c][t]), then broadcast (C1)."""
-        if self.rank == 0:
-            assert host_block is not None
-            self.block[:, : self.num_samples].copy_(host_block, non_blocking=True)
-        broadcast_input(self.block, src=0)
+        with torch.cuda.stream(self.stream):
+            if self.rank == 0:
+                assert host_block is not None
+                self.block[:, : self.num_samples].copy_(host_block, non_blocking=True)
+            broadcast_input(self.block, src=0)
 
     def run(self) -> torch.Tensor:
+        """One pass of this rank's DM range, enqueued on self.stream."""
         self.plan.execute(self.block.data_ptr(), self.out.data_ptr())
         return self.out
 
     def gather(self) -> Optional[torch.Tensor]:
-        return gather_rows(self.out, self.num_dms, self.cfg.tile_dm())
+        with torch.cuda.stream(self.stream):
+            return gather_rows(self.out, self.num_dms, self.cfg.tile_dm())
