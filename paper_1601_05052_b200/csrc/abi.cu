@@ -422,10 +422,13 @@ namespace {
 constexpr uint32_t kSmemBudget = 112 * 1024;  // aim for 2 CTAs per SM
 
 // Staged-family geometry for a config: shared-memory slots, stage count.
+// `slack` floats per window: the register-window kernel reads up to SPAN
+// samples past a window (never added), which must stay inside the slot.
 bool smem_geometry(const dd_context* c, uint32_t tile_time, uint32_t tile_dm, uint32_t channels,
-                   uint32_t max_span, uint32_t* win_cap, uint32_t* rec_bytes, uint32_t* cps,
-                   uint32_t* nstage, uint32_t* smem) {
-  const uint64_t wc = (static_cast<uint64_t>(max_span) + tile_time + 6u + 3u) & ~3ull;
+                   uint32_t max_span, uint32_t slack, uint32_t* win_cap, uint32_t* rec_bytes,
+                   uint32_t* cps, uint32_t* nstage, uint32_t* smem) {
+  const uint64_t wc =
+      (static_cast<uint64_t>(max_span) + tile_time + slack + 6u + 3u) & ~3ull;
   const uint64_t rb = ddb::plan_rec_bytes(tile_dm);
   const uint64_t slot = rb + 4 * wc;
   const uint64_t limit = static_cast<uint64_t>(c->smem_optin);
@@ -471,13 +474,21 @@ dd_status dd_config_family(dd_context* c, const dd_config* k, uint32_t channels,
   (void)num_dms;
   (void)s;
   bool smem_ok = smem_variant_ok(k->work_dm, k->work_time, block);
+  const bool regwin_ok = regwin_shape_ok(k->work_dm, k->work_time, k->items_time, block);
   if (smem_ok) {
     uint32_t a, b, cc, d, e;
-    smem_ok = smem_geometry(c, tile_time, tile_dm, channels, max_span, &a, &b, &cc, &d, &e);
+    smem_ok = smem_geometry(c, tile_time, tile_dm, channels, max_span, 0, &a, &b, &cc, &d, &e);
   }
   switch (k->staging) {
     case DD_STAGING_AUTO:
-      *family = smem_ok ? DD_STAGING_SMEM : DD_STAGING_DIRECT;
+      *family = regwin_ok ? DD_STAGING_REGWIN : smem_ok ? DD_STAGING_SMEM : DD_STAGING_DIRECT;
+      return DD_OK;
+    case DD_STAGING_REGWIN:
+      if (!regwin_ok)
+        return fail(DD_ERR_INVALID_ARGUMENT,
+                    "staging=regwin: needs items_time % 32 == 0, <= 256 threads and an "
+                    "instantiated work_dm x work_time variant");
+      *family = DD_STAGING_REGWIN;
       return DD_OK;
     case DD_STAGING_SMEM:
       if (!smem_ok)
@@ -545,15 +556,17 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
   a.depth = std::min(a.depth, a.tiles_dm);
 
   const uint64_t block = static_cast<uint64_t>(k->items_time) * k->items_dm;
-  const bool want_smem = k->staging == DD_STAGING_AUTO || k->staging == DD_STAGING_SMEM;
-  const bool smem_possible = want_smem && in_pitch % 4 == 0 &&
-                             smem_variant_ok(k->work_dm, k->work_time, block);
-  if (k->staging == DD_STAGING_REGWIN) {
-    delete p;
-    return fail(DD_ERR_INVALID_ARGUMENT, "staging mode not available in this build");
+  const bool smem_shape = smem_variant_ok(k->work_dm, k->work_time, block);
+  const bool regwin_shape = regwin_shape_ok(k->work_dm, k->work_time, k->items_time, block);
+  bool staged = in_pitch % 4 == 0;
+  switch (k->staging) {
+    case DD_STAGING_AUTO: staged = staged && (smem_shape || regwin_shape); break;
+    case DD_STAGING_SMEM: staged = staged && smem_shape; break;
+    case DD_STAGING_REGWIN: staged = staged && regwin_shape; break;
+    default: staged = false;
   }
 
-  if (smem_possible) {
+  if (staged) {
     a.rec_bytes = ddb::plan_rec_bytes(a.tile_dm);
     const uint64_t rec_total = static_cast<uint64_t>(a.tiles_dm) * channels * a.rec_bytes;
     cudaError_t e = cudaMalloc(&p->d_rec, rec_total);
@@ -562,31 +575,49 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
     if (e == cudaSuccess) e = cudaMemsetAsync(c->d_scratch, 0, 16, c->stream);
     if (e == cudaSuccess)
       e = launch_plan(d_shifts, p->d_rec, c->d_scratch, d_sum, channels, a.tiles_dm, a.tile_dm,
-                      a.rec_bytes, c->stream);
+                      k->work_dm, a.rec_bytes, c->stream);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(scratch, c->d_scratch, 16, cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    p->max_span = scratch[0];
-    uint64_t span_sum = 0;
-    std::memcpy(&span_sum, scratch + 2, 8);
     if (e != cudaSuccess) {
       cudaFree(p->d_rec);
       delete p;
       return cuda_fail(e, "plan pre-pass");
     }
+    p->max_span = scratch[0];
+    p->group_span = scratch[1];
+    uint64_t span_sum = 0;
+    std::memcpy(&span_sum, scratch + 2, 8);
+
+    // AUTO: register windows when every warp group fits a jump table,
+    // otherwise the shared-memory kernel.
+    uint32_t family = k->staging;
+    if (family == DD_STAGING_AUTO)
+      family = regwin_shape && p->group_span <= 31 ? DD_STAGING_REGWIN
+               : smem_shape                         ? DD_STAGING_SMEM
+                                                    : DD_STAGING_REGWIN;
+    ddb::KernelFn fn = nullptr;
+    uint32_t slack = 0;
+    if (family == DD_STAGING_REGWIN) {
+      fn = find_regwin_kernel(k->work_dm, k->work_time, p->group_span, &p->regwin_span);
+      slack = p->regwin_span + 4;
+    } else {
+      fn = find_smem_kernel(k->work_dm, k->work_time);
+    }
     uint32_t win_cap = 0, rec_bytes = 0, cps = 0, nstage = 0, smem = 0;
-    if (smem_geometry(c, a.tile_time, a.tile_dm, channels, p->max_span, &win_cap, &rec_bytes,
-                      &cps, &nstage, &smem)) {
+    if (fn != nullptr && smem_geometry(c, a.tile_time, a.tile_dm, channels, p->max_span, slack,
+                                       &win_cap, &rec_bytes, &cps, &nstage, &smem)) {
       a.win_cap = win_cap;
       a.cps = cps;
       a.nstage = nstage;
       a.rec = p->d_rec;
-      p->smem_fn = find_smem_kernel(k->work_dm, k->work_time);
+      p->smem_fn = fn;
       p->smem = smem;
-      p->threads = static_cast<uint32_t>(block);
+      // whole consumer warps plus one producer warp (dedisp.cu staged_loop)
+      p->threads = static_cast<uint32_t>(((block + 31) & ~31ull) + 32);
       const uint64_t groups_dm = (a.tiles_dm + a.depth - 1) / a.depth;
       p->blocks = static_cast<uint32_t>(groups_dm * a.tiles_time);
-      p->family = DD_STAGING_SMEM;
+      p->family = family;
       e = prepare_smem(p->smem_fn, smem);
       if (e != cudaSuccess) {
         cudaFree(p->d_rec);
@@ -602,11 +633,12 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
     cudaFree(p->d_rec);
     p->d_rec = nullptr;
   }
-  if (k->staging == DD_STAGING_SMEM) {
+  if (k->staging == DD_STAGING_SMEM || k->staging == DD_STAGING_REGWIN) {
     delete p;
     return fail(DD_ERR_INVALID_ARGUMENT,
-                "staging=smem: no staged kernel for this config (work_dm x work_time variant, "
-                "block size, input pitch or shared-memory window)");
+                std::string("staging=") + (k->staging == DD_STAGING_SMEM ? "smem" : "regwin") +
+                    ": no staged kernel for this config (work_dm x work_time variant, block "
+                    "size, items_time, input pitch or shared-memory window)");
   }
   // Direct family: pack small tiles, virtualise oversize blocks.
   const uint32_t bi = static_cast<uint32_t>(std::min<uint64_t>(block, 0xffffffffull));
@@ -672,7 +704,7 @@ dd_status dd_plan_execute(dd_plan* p, const float* d_in, float* d_out, uint64_t 
   a.in = d_in;
   a.out = d_out;
   a.out_pitch = out_pitch;
-  if (p->family == DD_STAGING_SMEM) {
+  if (p->family == DD_STAGING_SMEM || p->family == DD_STAGING_REGWIN) {
     if ((reinterpret_cast<uintptr_t>(d_in) & 15u) != 0)
       return fail(DD_ERR_INVALID_ARGUMENT, "staged kernels need a 16-byte aligned input");
     DD_CUDA(launch_smem(p->smem_fn, a, p->blocks, p->threads, p->smem, c->stream));

@@ -31,7 +31,7 @@ struct dd_plan {
   void (*smem_fn)(const ddb::TiledArgs) = nullptr;
   uint32_t blocks = 0, threads = 0, smem = 0;
   uint32_t grid_y = 1;
-  uint32_t max_span = 0, max_delay = 0;
+  uint32_t max_span = 0, max_delay = 0, group_span = 0, regwin_span = 0;
   uint64_t staged_bytes = 0;
 };
 
@@ -47,18 +47,22 @@ cudaError_t launch_delay_table(uint32_t* d_shifts, uint32_t* d_max, uint32_t num
                                uint32_t channels, uint32_t dm_offset, double f_min, double width,
                                double dm_first, double dm_step, double rate, cudaStream_t st);
 cudaError_t launch_plan(const uint32_t* d_shifts, uint8_t* d_rec, uint32_t* d_max_span,
-                        unsigned long long* d_span_sum, uint32_t channels, uint32_t tiles_dm, uint32_t tile_dm,
-                        uint32_t rec_bytes, cudaStream_t st);
+                        unsigned long long* d_span_sum, uint32_t channels, uint32_t tiles_dm,
+                        uint32_t tile_dm, uint32_t group, uint32_t rec_bytes, cudaStream_t st);
 cudaError_t launch_max_u32(const uint32_t* d_v, uint64_t n, uint32_t* d_out, cudaStream_t st);
 
 using KernelFn = void (*)(const TiledArgs);
 // Staged-kernel variant for work_dm x work_time; nullptr when not
 // instantiated.  *max_threads = the variant's block-size cap.
 KernelFn find_smem_kernel(uint32_t k, uint32_t w, uint32_t* max_threads = nullptr);
+// Register-window variant for (work_dm, work_time) covering group_span
+// (or the widest one); *span_out = its SPAN.  nullptr when not instantiated.
+KernelFn find_regwin_kernel(uint32_t k, uint32_t w, uint32_t group_span, uint32_t* span_out);
+bool regwin_shape_ok(uint32_t k, uint32_t w, uint32_t items_time, uint64_t block);
 // True when the staged family can run cfg (block size within the variant's cap).
 inline bool smem_variant_ok(uint32_t k, uint32_t w, uint64_t block) {
   uint32_t cap = 0;
-  return find_smem_kernel(k, w, &cap) != nullptr && block <= cap;
+  return find_smem_kernel(k, w, &cap) != nullptr && ((block + 31) & ~31ull) <= cap;
 }
 cudaError_t launch_reference(const float* in, uint64_t pitch, const uint32_t* shifts, float* out,
                              uint64_t out_pitch, uint32_t channels, uint32_t s, uint32_t num_dms,

@@ -44,13 +44,15 @@ __global__ void k_delay_table(uint32_t* __restrict__ shifts, uint32_t* __restric
 // shifts with no ordering assumed (the reference's kernels.cpp:147-156 and
 // count_loads.cpp:36-42 make the same choice), writes the record and folds
 // the span into a global maximum used to size shared memory.
+// max_span[0] = widest tile span; max_span[1] = widest spread of any aligned
+// group of `group` consecutive DMs (the register-window kernel's warp rows).
 __global__ void k_plan(const uint32_t* __restrict__ shifts, uint8_t* __restrict__ rec,
                        uint32_t* __restrict__ max_span, unsigned long long* __restrict__ span_sum,
-                       uint32_t channels, uint32_t tiles_dm, uint32_t tile_dm,
+                       uint32_t channels, uint32_t tiles_dm, uint32_t tile_dm, uint32_t group,
                        uint32_t rec_bytes) {
   const uint64_t n = static_cast<uint64_t>(tiles_dm) * channels;
   const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  uint32_t span = 0;
+  uint32_t span = 0, gspan = 0;
   if (i < n) {
     const uint32_t b = static_cast<uint32_t>(i / channels);
     const uint32_t ch = static_cast<uint32_t>(i - static_cast<uint64_t>(b) * channels);
@@ -67,12 +69,23 @@ __global__ void k_plan(const uint32_t* __restrict__ shifts, uint8_t* __restrict_
     r[1] = span;
     r[2] = 0;
     r[3] = 0;
-    for (uint32_t l = 0; l < tile_dm; ++l) r[4 + l] = col[static_cast<uint64_t>(l) * channels] - lo;
+    for (uint32_t g0 = 0; g0 < tile_dm; g0 += group) {
+      uint32_t glo = 0xffffffffu, ghi = 0;
+      for (uint32_t l = g0; l < g0 + group && l < tile_dm; ++l) {
+        const uint32_t v = col[static_cast<uint64_t>(l) * channels];
+        r[4 + l] = v - lo;
+        glo = min(glo, v);
+        ghi = max(ghi, v);
+      }
+      gspan = max(gspan, ghi - glo);
+    }
   }
   const uint32_t sum = __reduce_add_sync(0xffffffffu, span);
   span = __reduce_max_sync(0xffffffffu, span);
+  gspan = __reduce_max_sync(0xffffffffu, gspan);
   if ((threadIdx.x & 31) == 0) {
     atomicMax(max_span, span);
+    atomicMax(max_span + 1, gspan);
     atomicAdd(span_sum, static_cast<unsigned long long>(sum));
   }
 }
@@ -109,14 +122,14 @@ cudaError_t launch_delay_table(uint32_t* d_shifts, uint32_t* d_max, uint32_t num
 }
 
 cudaError_t launch_plan(const uint32_t* d_shifts, uint8_t* d_rec, uint32_t* d_max_span,
-                        unsigned long long* d_span_sum, uint32_t channels, uint32_t tiles_dm, uint32_t tile_dm,
-                        uint32_t rec_bytes, cudaStream_t st) {
+                        unsigned long long* d_span_sum, uint32_t channels, uint32_t tiles_dm,
+                        uint32_t tile_dm, uint32_t group, uint32_t rec_bytes, cudaStream_t st) {
   const uint64_t n = static_cast<uint64_t>(tiles_dm) * channels;
   const uint32_t threads = 128;
   const uint64_t blocks = (n + threads - 1) / threads;
   k_plan<<<static_cast<uint32_t>(blocks), threads, 0, st>>>(d_shifts, d_rec, d_max_span,
                                                             d_span_sum, channels, tiles_dm, tile_dm,
-                                                            rec_bytes);
+                                                            group ? group : 1, rec_bytes);
   return cudaGetLastError();
 }
 

@@ -151,10 +151,10 @@ dd_status dd_enumerate_configs(uint32_t num_dms, uint32_t s, const dd_limits* li
 
 // The GPU tuning space: reference-valid 4-tuples (so tuning records keep
 // the reference's config identity) that map onto whole
-// warps of the staged kernel -- items_time a multiple of 32, or 8/16 lanes
-// along time with the warp completed along DM -- with 64..1024 threads and
-// an instantiated work_dm x work_time variant; crossed with
-// dm_tile_depth in {1, 2, 4}.  The direct family is added for the same
+// warps -- items_time a multiple of 32, or 8/16 lanes along time with the
+// warp completed along DM.  Register-window shapes (K4) at depth {1, 2};
+// shared-memory shapes (K3, 64..1024 threads, instantiated work_dm x
+// work_time variant) at depth {1, 2, 4}; and the direct family for the same
 // shapes at depth 1 so the paper's "rely on the cache" option is measured.
 dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint32_t num_dms,
                                    const dd_limits* limits, dd_config* out, uint64_t capacity,
@@ -167,10 +167,19 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
   std::vector<dd_config> v;
   for (const dd_config& k : reference_space(num_dms, s, effective_limits(limits))) {
     const uint32_t block = k.items_time * k.items_dm;
-    if (block < 64 || block > 1024 || block % 32 != 0) continue;
+    if (block < 32 || block > 1024 || block % 32 != 0) continue;
     if (!(k.items_time % 32 == 0 || k.items_time == 8 || k.items_time == 16)) continue;
-    if (!smem_variant_ok(k.work_dm, k.work_time, block)) continue;
     const uint32_t tiles_dm = num_dms / (k.items_dm * k.work_dm);
+    if (regwin_shape_ok(k.work_dm, k.work_time, k.items_time, block)) {
+      for (uint32_t depth : {1u, 2u}) {
+        if (depth > 1 && tiles_dm < depth * 2) continue;
+        dd_config c = k;
+        c.dm_tile_depth = depth;
+        c.staging = DD_STAGING_REGWIN;
+        v.push_back(c);
+      }
+    }
+    if (block < 64 || !smem_variant_ok(k.work_dm, k.work_time, block)) continue;
     for (uint32_t depth : {1u, 2u, 4u}) {
       if (depth > 1 && tiles_dm < depth * 2) continue;
       dd_config c = k;

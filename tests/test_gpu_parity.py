@@ -81,6 +81,11 @@ APERTIF_CFGS = [
     (K(800, 1, 1, 1), 1, "smem"),
     (K(125, 8, 8, 1), 1, "direct"),         # the reference's CPU config
     (K(16, 4, 5, 8), 1, "auto"),
+    (K(32, 4, 25, 4), 1, "regwin"),
+    (K(32, 8, 5, 8), 1, "regwin"),
+    (K(160, 1, 5, 4), 2, "regwin"),
+    (K(32, 2, 25, 2), 1, "regwin"),
+    (K(32, 1, 5, 16), 1, "regwin"),
 ]
 
 
@@ -98,7 +103,8 @@ def test_apertif_64_golden(dev, golden, cfg, depth, staging):
 
 
 @pytest.mark.parametrize("cfg,staging", [(None, "auto"), (K(32, 4, 5, 1), "smem"),
-                                         (K(64, 4, 1, 4), "smem"), (K(1000, 1, 1, 4), "direct")])
+                                         (K(64, 4, 1, 4), "smem"), (K(1000, 1, 1, 4), "direct"),
+                                         (K(32, 4, 25, 4), "regwin"), (K(64, 2, 5, 8), "regwin")])
 def test_lofar_64_golden(dev, golden, cfg, staging):
     g = golden["baseline"][1]
     setup, table, fb = _golden_instance(g)
@@ -119,8 +125,10 @@ def test_two_dm_golden(dev, golden, idx):
 def test_apertif_4096_golden(dev, golden):
     g = golden["baseline"][2]
     setup, table, fb = _golden_instance(g)
-    for cfg, depth in ((K(32, 8, 1, 8), 1), (K(160, 1, 5, 8), 2)):
-        out = api.dedisperse_tiled(fb, table, cfg, api.ExecOptions(dm_tile_depth=depth))
+    for cfg, depth, st in ((K(32, 8, 1, 8), 1, "smem"), (K(160, 1, 5, 8), 2, "smem"),
+                           (K(32, 4, 25, 4), 1, "regwin"), (K(32, 8, 5, 8), 2, "regwin")):
+        out = api.dedisperse_tiled(fb, table, cfg, api.ExecOptions(dm_tile_depth=depth,
+                                                                   staging=st))
         assert O.fnv1a(out.data) == g["out_fnv"], cfg
 
 
@@ -200,9 +208,21 @@ def test_non_monotone_and_fault_injected_tables(dev, golden):
     t = ((320 + int(sh.max()) + 319) // 320) * 320
     fb = api.noise_filterbank(setup, t, 1.0, 5)
     ref = O.dedisperse_reference(fb.data, sh, 320)
-    for cfg, st in ((K(32, 4, 5, 2), "smem"), (K(160, 2, 1, 16), "smem"), (K(32, 8, 1, 4), "direct")):
+    for cfg, st in ((K(32, 4, 5, 2), "smem"), (K(160, 2, 1, 16), "smem"),
+                    (K(32, 8, 1, 4), "direct"), (K(32, 2, 5, 8), "regwin")):
         out = api.dedisperse_tiled(fb, table, cfg, api.ExecOptions(staging=st))
         assert np.array_equal(_bits(out.data), _bits(ref)), cfg
+    # near-monotone table with jitter: register-window fast and slow paths mix
+    base = (np.arange(d)[:, None] * np.linspace(9, 0, 24)[None, :]).astype(np.int64)
+    jit = rng.integers(0, 3, size=(d, 24)) * rng.integers(0, 2, size=(d, 24)) * 7
+    sh2 = (base + jit).astype(np.uint32)
+    table2 = api.DelayTable(setup, d, sh2, int(sh2.max()))
+    t2 = ((320 + int(sh2.max()) + 319) // 320) * 320
+    fb2 = api.noise_filterbank(setup, t2, 1.0, 6)
+    ref2 = O.dedisperse_reference(fb2.data, sh2, 320)
+    for cfg in (K(32, 2, 5, 4), K(32, 1, 5, 8), K(32, 1, 5, 16)):
+        out = api.dedisperse_tiled(fb2, table2, cfg, api.ExecOptions(staging="regwin"))
+        assert np.array_equal(_bits(out.data), _bits(ref2)), cfg
     # dedisp_tune.cpp:278-287 analogue: one corrupted entry must change the output
     g = golden["baseline"][0]
     setup, table, fb = _golden_instance(g)
