@@ -70,7 +70,7 @@ typedef enum dd_staging {
 
 /* KernelConfig (kernels.hpp:40-52) plus the two GPU knobs of the north star:
  * dm_tile_depth = DM tiles one CTA walks in sequence (0 or 1 = one), and the
- * staging strategy. */
+ * staging strategy; `flags` selects GPU-only relaxations. */
 typedef struct dd_config {
   uint32_t items_time;
   uint32_t items_dm;
@@ -78,7 +78,19 @@ typedef struct dd_config {
   uint32_t work_dm;
   uint32_t dm_tile_depth;
   uint32_t staging; /* dd_staging */
+  uint32_t flags;   /* DD_CONFIG_* */
 } dd_config;
+
+/* GPU tiling: tile_time (items_time*work_time) need not divide s -- the
+ * last time tile is predicated.  Only the staged families accept it; the
+ * reference-compatible entry points (dd_validate_config without the flag,
+ * dd_dedisperse) keep the reference's exact-division rule. */
+#define DD_CONFIG_GPU_TILING 0x1u
+/* Staged families: channels per pipeline stage in bits 8..11 (1..8; 0 lets
+ * the plan choose).  A tuning knob: larger stages amortise the per-stage
+ * synchronisation, smaller ones leave shared memory for more CTAs per SM. */
+#define DD_CONFIG_CPS_SHIFT 8u
+#define DD_CONFIG_CPS_MASK (0xfu << DD_CONFIG_CPS_SHIFT)
 
 /* KernelLimits (kernels.hpp:31-34); {0,0} means the reference defaults
  * {1024, 256}. */

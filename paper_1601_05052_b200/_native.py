@@ -16,6 +16,9 @@ LIB_PATH = os.path.join(PKG, "libdedisp_b200.so")
 DD_OK, DD_ERR_INVALID_ARGUMENT, DD_ERR_CAPACITY, DD_ERR_CUDA, DD_ERR_NO_DEVICE, DD_ERR_INTERNAL = range(6)
 STAGING = {"auto": 0, "smem": 1, "direct": 2, "regwin": 3}
 STAGING_NAME = {v: k for k, v in STAGING.items()}
+DD_CONFIG_GPU_TILING = 0x1
+DD_CONFIG_CPS_SHIFT = 8
+DD_CONFIG_CPS_MASK = 0xF << DD_CONFIG_CPS_SHIFT
 
 
 class CapacityError(RuntimeError):
@@ -35,11 +38,12 @@ class dd_setup(C.Structure):
 class dd_config(C.Structure):
     _fields_ = [("items_time", C.c_uint32), ("items_dm", C.c_uint32),
                 ("work_time", C.c_uint32), ("work_dm", C.c_uint32),
-                ("dm_tile_depth", C.c_uint32), ("staging", C.c_uint32)]
+                ("dm_tile_depth", C.c_uint32), ("staging", C.c_uint32),
+                ("flags", C.c_uint32)]
 
     def tuple(self):
         return (self.items_time, self.items_dm, self.work_time, self.work_dm,
-                self.dm_tile_depth, self.staging)
+                self.dm_tile_depth, self.staging, self.flags)
 
 
 class dd_limits(C.Structure):

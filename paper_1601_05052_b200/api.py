@@ -233,9 +233,11 @@ class LoadCounts:
     ideal_loads: int
 
 
-def _cfg(cfg: KernelConfig, depth: int = 1, staging: str = "auto") -> N.dd_config:
+def _cfg(cfg: KernelConfig, depth: int = 1, staging: str = "auto",
+         gpu_tiling: bool = False, stage_channels: int = 0) -> N.dd_config:
+    flags = (N.DD_CONFIG_GPU_TILING if gpu_tiling else 0) | (stage_channels << N.DD_CONFIG_CPS_SHIFT)
     return N.dd_config(cfg.items_time, cfg.items_dm, cfg.work_time, cfg.work_dm, depth,
-                       N.STAGING[staging])
+                       N.STAGING[staging], flags)
 
 
 def config_valid(cfg: KernelConfig, num_dms: int, samples_per_second: int,
@@ -366,20 +368,23 @@ class Context:
     def plan(self, d_shifts: int, channels: int, num_dms: int, samples_per_second: int,
              num_samples: int, in_pitch: int, cfg: Optional[KernelConfig] = None,
              dm_tile_depth: int = 1, staging: str = "auto",
-             limits: KernelLimits = KernelLimits()) -> "Plan":
+             limits: KernelLimits = KernelLimits(), gpu_tiling: bool = False,
+             stage_channels: int = 0) -> "Plan":
+        """gpu_tiling: tile_time need not divide s (staged families only);
+        stage_channels: channels per pipeline stage (0 = plan's choice)."""
         return Plan(self, d_shifts, channels, num_dms, samples_per_second, num_samples, in_pitch,
-                    cfg, dm_tile_depth, staging, limits)
+                    cfg, dm_tile_depth, staging, limits, gpu_tiling, stage_channels)
 
 
 class Plan:
     """dd_plan: a table + config bound to one kernel launch."""
 
     def __init__(self, ctx: Context, d_shifts, channels, num_dms, s, num_samples, in_pitch,
-                 cfg, depth, staging, limits):
+                 cfg, depth, staging, limits, gpu_tiling=False, stage_channels=0):
         self.ctx = ctx
         self.num_dms, self.s, self.channels = num_dms, s, channels
         h = C.c_void_p()
-        kc = _cfg(cfg, depth, staging) if cfg is not None else None
+        kc = _cfg(cfg, depth, staging, gpu_tiling, stage_channels) if cfg is not None else None
         check(lib().dd_plan_create(ctx.handle, C.c_void_p(d_shifts), channels, num_dms, s,
                                    num_samples, in_pitch, C.byref(kc) if kc is not None else None,
                                    C.byref(limits.c()), C.byref(h)))
@@ -443,10 +448,16 @@ class TuningRecord:
     dm_tile_depth: int = 1
     staging: str = "auto"
     family: str = ""
+    flags: int = 0  # DD_CONFIG_* (GPU tiling, channels per stage)
+
+    @property
+    def stage_channels(self) -> int:
+        return (self.flags & N.DD_CONFIG_CPS_MASK) >> N.DD_CONFIG_CPS_SHIFT
 
     def c(self) -> N.dd_tuning_record:
         r = N.dd_tuning_record()
         r.config = _cfg(self.config, self.dm_tile_depth, self.staging)
+        r.config.flags = self.flags
         r.mean_time = self.mean_time
         r.gflops = self.gflops
         return r
@@ -506,7 +517,7 @@ def enumerate_gpu_configs(setup: ObservationSetup, num_dms: int,
     check(lib().dd_enumerate_gpu_configs(ctx.handle, C.byref(setup.c()), num_dms,
                                          C.byref(limits.c()), buf, n.value, C.byref(n)))
     return [(KernelConfig(b.items_time, b.items_dm, b.work_time, b.work_dm), b.dm_tile_depth,
-             N.STAGING_NAME[b.staging]) for b in buf[:n.value]]
+             N.STAGING_NAME[b.staging], b.flags) for b in buf[:n.value]]
 
 
 def select_best(records: Sequence[TuningRecord]) -> int:
@@ -555,7 +566,7 @@ def _sweep(setup, num_dms, limits, repeats, seed, zero, full_space, max_configs,
         out.append(TuningRecord(KernelConfig(k.items_time, k.items_dm, k.work_time, k.work_dm),
                                 [], r.mean_time, r.gflops, bool(r.timer_warning),
                                 k.dm_tile_depth, N.STAGING_NAME[k.staging],
-                                N.STAGING_NAME.get(r.family, "")))
+                                N.STAGING_NAME.get(r.family, ""), k.flags))
     return TuningResult(setup, num_dms, zero, limits, repeats, seed, out, summ.best_index,
                         _stats(summ), summ.realtime_threshold_gflops, bool(summ.realtime_pass))
 
@@ -598,12 +609,12 @@ def best_fixed_config(results: Sequence[TuningResult]) -> FixedConfigReport:
     by = {}
     for i, r in enumerate(results):
         for rec in r.records:
-            key = (rec.config, rec.dm_tile_depth, rec.staging)
+            key = (rec.config, rec.dm_tile_depth, rec.staging, rec.flags)
             v = by.setdefault(key, [])
             if len(v) == i:
                 v.append(rec.gflops)
     best = None
-    for key in sorted(by, key=lambda k: (k[0], k[1], k[2])):
+    for key in sorted(by, key=lambda k: (k[0], k[1], k[2], k[3])):
         v = by[key]
         if len(v) != len(results):
             continue

@@ -20,7 +20,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdedisp_b200.so")
 SOURCES = ["table.cu", "dedisp.cu", "abi.cu", "tuner.cu", "host.cpp"]
-HEADERS = ["common.cuh", "internal.hpp"]
+HEADERS = ["common.cuh", "internal.hpp", "regwin_dispatch.cuh"]
 PUBLIC = [os.path.join(ROOT, "include", "dedisp_b200.h"),
           os.path.join(ROOT, "include", "dedisp", "b200.hpp")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -42,7 +42,18 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+def gen_dispatch() -> None:
+    """Regenerate csrc/regwin_dispatch.cuh when its generator changed."""
+    gen = os.path.join(CSRC, "gen_dispatch.py")
+    out = os.path.join(CSRC, "regwin_dispatch.cuh")
+    if _stale(out, [gen]):
+        r = subprocess.run([sys.executable, gen], capture_output=True, text=True, check=True)
+        with open(out, "w") as f:
+            f.write(r.stdout)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    gen_dispatch()
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
     deps_common = [os.path.join(CSRC, h) for h in HEADERS] + PUBLIC + [__file__]

@@ -3,6 +3,7 @@
 // tables, dedispersion plans and the host-buffer drop-in entry points.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -356,9 +357,12 @@ dd_status dd_validate_config(const dd_config* k, uint32_t num_dms, uint32_t s,
     return fail(DD_ERR_INVALID_ARGUMENT, "kernel config parameters must all be positive");
   const uint64_t tt = static_cast<uint64_t>(k->items_time) * k->work_time;
   const uint64_t td = static_cast<uint64_t>(k->items_dm) * k->work_dm;
-  if (tt > s || s % tt != 0)
+  const bool gpu_tiling = (k->flags & DD_CONFIG_GPU_TILING) != 0;
+  if (!gpu_tiling && (tt > s || s % tt != 0))
     return fail(DD_ERR_INVALID_ARGUMENT, "items_time * work_time = " + std::to_string(tt) +
                                              " does not divide s = " + std::to_string(s));
+  if (gpu_tiling && tt > 0xffffffffull)
+    return fail(DD_ERR_INVALID_ARGUMENT, "tile_time overflows");
   if (td > num_dms || num_dms % td != 0)
     return fail(DD_ERR_INVALID_ARGUMENT, "items_dm * work_dm = " + std::to_string(td) +
                                              " does not divide the trial count " +
@@ -370,6 +374,10 @@ dd_status dd_validate_config(const dd_config* k, uint32_t num_dms, uint32_t s,
     return fail(DD_ERR_INVALID_ARGUMENT, "work_time * work_dm exceeds the accumulator limit of " +
                                              std::to_string(L.max_accumulators));
   if (k->staging > DD_STAGING_REGWIN) return fail(DD_ERR_INVALID_ARGUMENT, "unknown staging mode");
+  if (k->flags & ~(DD_CONFIG_GPU_TILING | DD_CONFIG_CPS_MASK))
+    return fail(DD_ERR_INVALID_ARGUMENT, "unknown config flags");
+  if (((k->flags & DD_CONFIG_CPS_MASK) >> DD_CONFIG_CPS_SHIFT) > 8)
+    return fail(DD_ERR_INVALID_ARGUMENT, "channels per stage must be 1..8");
   return DD_OK;
 }
 
@@ -425,8 +433,8 @@ constexpr uint32_t kSmemBudget = 112 * 1024;  // aim for 2 CTAs per SM
 // `slack` floats per window: the register-window kernel reads up to SPAN
 // samples past a window (never added), which must stay inside the slot.
 bool smem_geometry(const dd_context* c, uint32_t tile_time, uint32_t tile_dm, uint32_t channels,
-                   uint32_t max_span, uint32_t slack, uint32_t* win_cap, uint32_t* rec_bytes,
-                   uint32_t* cps, uint32_t* nstage, uint32_t* smem) {
+                   uint32_t max_span, uint32_t slack, uint32_t want_cps, uint32_t* win_cap,
+                   uint32_t* rec_bytes, uint32_t* cps, uint32_t* nstage, uint32_t* smem) {
   const uint64_t wc =
       (static_cast<uint64_t>(max_span) + tile_time + slack + 6u + 3u) & ~3ull;
   const uint64_t rb = ddb::plan_rec_bytes(tile_dm);
@@ -434,9 +442,20 @@ bool smem_geometry(const dd_context* c, uint32_t tile_time, uint32_t tile_dm, ui
   const uint64_t limit = static_cast<uint64_t>(c->smem_optin);
   // Prefer 3 stages of several channels within the 2-CTA budget; degrade
   // to fewer channels, then to 2 stages, then to the opt-in maximum.
-  const uint32_t cps_opts[] = {8, 4, 2, 1};
+  // DEDISP_B200_STAGE_CPS / _NSTAGE pin the shape (tuning experiments).
+  uint32_t cps_opts[] = {8, 4, 2, 1};
+  uint32_t ns_opts[] = {3, 2};
+  if (want_cps >= 1 && want_cps <= 8) cps_opts[0] = want_cps;
+  if (const char* e = std::getenv("DEDISP_B200_STAGE_CPS")) {
+    const uint32_t v = static_cast<uint32_t>(std::atoi(e));
+    if (v >= 1 && v <= 8) cps_opts[0] = v;
+  }
+  if (const char* e = std::getenv("DEDISP_B200_STAGE_NSTAGE")) {
+    const uint32_t v = static_cast<uint32_t>(std::atoi(e));
+    if (v >= 2 && v <= 4) ns_opts[0] = v;
+  }
   for (uint64_t budget : {static_cast<uint64_t>(kSmemBudget), limit}) {
-    for (uint32_t ns : {3u, 2u}) {
+    for (uint32_t ns : ns_opts) {
       for (uint32_t cp : cps_opts) {
         if (cp > channels && cp != 1) continue;
         const uint64_t bytes = 128 + static_cast<uint64_t>(ns) * cp * slot;
@@ -477,7 +496,9 @@ dd_status dd_config_family(dd_context* c, const dd_config* k, uint32_t channels,
   const bool regwin_ok = regwin_shape_ok(k->work_dm, k->work_time, k->items_time, block);
   if (smem_ok) {
     uint32_t a, b, cc, d, e;
-    smem_ok = smem_geometry(c, tile_time, tile_dm, channels, max_span, 0, &a, &b, &cc, &d, &e);
+    smem_ok = smem_geometry(c, tile_time, tile_dm, channels, max_span, 0,
+                            (k->flags & DD_CONFIG_CPS_MASK) >> DD_CONFIG_CPS_SHIFT, &a, &b,
+                            &cc, &d, &e);
   }
   switch (k->staging) {
     case DD_STAGING_AUTO:
@@ -550,7 +571,7 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
   a.work_dm = k->work_dm;
   a.tile_time = k->items_time * k->work_time;
   a.tile_dm = k->items_dm * k->work_dm;
-  a.tiles_time = s / a.tile_time;
+  a.tiles_time = (s + a.tile_time - 1) / a.tile_time;  // last tile predicated (GPU tiling)
   a.tiles_dm = num_dms / a.tile_dm;
   a.depth = std::max<uint32_t>(1, k->dm_tile_depth);
   a.depth = std::min(a.depth, a.tiles_dm);
@@ -570,17 +591,20 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
     a.rec_bytes = ddb::plan_rec_bytes(a.tile_dm);
     const uint64_t rec_total = static_cast<uint64_t>(a.tiles_dm) * channels * a.rec_bytes;
     cudaError_t e = cudaMalloc(&p->d_rec, rec_total);
+    if (e == cudaSuccess)
+      e = cudaMalloc(&p->d_ls, static_cast<uint64_t>(a.tiles_dm) * channels * sizeof(uint2));
     uint32_t scratch[4] = {0, 0, 0, 0};
     unsigned long long* d_sum = reinterpret_cast<unsigned long long*>(c->d_scratch + 2);
     if (e == cudaSuccess) e = cudaMemsetAsync(c->d_scratch, 0, 16, c->stream);
     if (e == cudaSuccess)
-      e = launch_plan(d_shifts, p->d_rec, c->d_scratch, d_sum, channels, a.tiles_dm, a.tile_dm,
+      e = launch_plan(d_shifts, p->d_rec, p->d_ls, c->d_scratch, d_sum, channels, a.tiles_dm, a.tile_dm,
                       k->work_dm, a.rec_bytes, c->stream);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(scratch, c->d_scratch, 16, cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
       cudaFree(p->d_rec);
+      cudaFree(p->d_ls);
       delete p;
       return cuda_fail(e, "plan pre-pass");
     }
@@ -605,22 +629,32 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
       fn = find_smem_kernel(k->work_dm, k->work_time);
     }
     uint32_t win_cap = 0, rec_bytes = 0, cps = 0, nstage = 0, smem = 0;
-    if (fn != nullptr && smem_geometry(c, a.tile_time, a.tile_dm, channels, p->max_span, slack,
-                                       &win_cap, &rec_bytes, &cps, &nstage, &smem)) {
+    // the launch must fit the variant's register budget
+    const uint32_t threads = static_cast<uint32_t>(((block + 31) & ~31ull) + 32);
+    cudaFuncAttributes fattr{};
+    if (fn != nullptr && (cudaFuncGetAttributes(&fattr, fn) != cudaSuccess ||
+                          static_cast<uint32_t>(fattr.maxThreadsPerBlock) < threads))
+      fn = nullptr;
+    if (fn != nullptr &&
+        smem_geometry(c, a.tile_time, a.tile_dm, channels, p->max_span, slack,
+                      (k->flags & DD_CONFIG_CPS_MASK) >> DD_CONFIG_CPS_SHIFT, &win_cap,
+                      &rec_bytes, &cps, &nstage, &smem)) {
       a.win_cap = win_cap;
       a.cps = cps;
       a.nstage = nstage;
       a.rec = p->d_rec;
+      a.ls = p->d_ls;
       p->smem_fn = fn;
       p->smem = smem;
       // whole consumer warps plus one producer warp (dedisp.cu staged_loop)
-      p->threads = static_cast<uint32_t>(((block + 31) & ~31ull) + 32);
+      p->threads = threads;
       const uint64_t groups_dm = (a.tiles_dm + a.depth - 1) / a.depth;
       p->blocks = static_cast<uint32_t>(groups_dm * a.tiles_time);
       p->family = family;
       e = prepare_smem(p->smem_fn, smem);
       if (e != cudaSuccess) {
         cudaFree(p->d_rec);
+        cudaFree(p->d_ls);
         delete p;
         return cuda_fail(e, "cudaFuncSetAttribute");
       }
@@ -631,9 +665,12 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
       return DD_OK;
     }
     cudaFree(p->d_rec);
+    cudaFree(p->d_ls);
     p->d_rec = nullptr;
+    p->d_ls = nullptr;
   }
-  if (k->staging == DD_STAGING_SMEM || k->staging == DD_STAGING_REGWIN) {
+  if (k->staging == DD_STAGING_SMEM || k->staging == DD_STAGING_REGWIN ||
+      (k->flags & DD_CONFIG_GPU_TILING && s % a.tile_time != 0)) {
     delete p;
     return fail(DD_ERR_INVALID_ARGUMENT,
                 std::string("staging=") + (k->staging == DD_STAGING_SMEM ? "smem" : "regwin") +
@@ -662,6 +699,7 @@ dd_status dd_plan_destroy(dd_plan* p) {
   if (p->d_rec) {
     cudaSetDevice(p->ctx->device);
     cudaFree(p->d_rec);
+    cudaFree(p->d_ls);
   }
   delete p;
   return DD_OK;

@@ -51,6 +51,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Producer-side wait: try_wait with a suspend-time hint parks the lane in
+// hardware until the phase completes (or the hint expires) instead of
+// polling, so the waiting producer does not steal issue slots from the
+// consumer warps of its scheduler.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+  }
+}
+
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` in bytes.
 // dst/src 16-byte aligned, bytes a multiple of 16 (SASS: UBLKCP.S.G).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
@@ -97,6 +114,7 @@ struct TiledArgs {
   const float* in;
   uint64_t in_pitch;  // floats, multiple of 4 for the staged families
   const uint8_t* rec; // [tiles_dm][channels] records, rec_bytes each
+  const uint2* ls;    // [tiles_dm][channels] (lo, span), compact copy for the producer
   const uint32_t* shifts;  // DM-major table (direct family)
   float* out;
   uint64_t out_pitch;  // floats

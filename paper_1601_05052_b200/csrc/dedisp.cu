@@ -8,6 +8,7 @@
 // kernel here is bit-identical to dedisperse_reference.  Build flags must
 // not enable fast-math / FTZ (see build.py).
 #include "common.cuh"
+#include "regwin_dispatch.cuh"
 
 namespace ddb {
 
@@ -116,9 +117,27 @@ __device__ __forceinline__ Pipe pipe_setup(const TiledArgs& a, uint8_t* smem) {
   return p;
 }
 
+// (lo, span) of the up-to-8 channels of chunk g, fetched one chunk ahead
+// by the producer so the global-memory latency overlaps its slot wait.
+struct ChunkSpans {
+  uint2 v[8];
+};
+
+__device__ __forceinline__ ChunkSpans pipe_spans(const TiledArgs& a, const Pipe& p, uint32_t g) {
+  ChunkSpans c;
+  const uint32_t b = p.b_first + g / p.nchunk;
+  const uint32_t ch0 = (g % p.nchunk) * a.cps;
+  const uint32_t ncs = min(a.cps, a.channels - ch0);
+  const uint2* src = a.ls + static_cast<uint64_t>(b) * a.channels + ch0;
+#pragma unroll
+  for (uint32_t cc = 0; cc < 8; ++cc) c.v[cc] = cc < ncs ? __ldg(src + cc) : make_uint2(0, 0);
+  return c;
+}
+
 // Stage chunk g = (tile, channel group) into its slot: one bulk copy for the
 // chunk's plan records, one per channel window, all counted on full[slot].
-__device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, uint32_t g) {
+__device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, uint32_t g,
+                                           const ChunkSpans& cs) {
   const uint32_t b = p.b_first + g / p.nchunk;
   const uint32_t ch0 = (g % p.nchunk) * a.cps;
   const uint32_t ncs = min(a.cps, a.channels - ch0);
@@ -128,13 +147,13 @@ __device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, ui
   uint32_t total = ncs * a.rec_bytes;
 #pragma unroll
   for (uint32_t cc = 0; cc < 8; ++cc) {
-    if (cc < ncs) {
-      const uint32_t* r = reinterpret_cast<const uint32_t*>(rsrc + cc * a.rec_bytes);
-      const uint32_t lo = __ldg(r), span = __ldg(r + 1);
-      start[cc] = (p.t0 + lo) & ~3u;
-      bytes[cc] = (((p.t0 + lo + span + a.tile_time + 3u) & ~3u) - start[cc]) * 4u;
-      total += bytes[cc];
-    }
+    const uint32_t lo = cs.v[cc].x, span = cs.v[cc].y;
+    start[cc] = (p.t0 + lo) & ~3u;
+    // a predicated last time tile must not read past the (pitched) row
+    const uint32_t end = min((p.t0 + lo + span + a.tile_time + 3u) & ~3u,
+                             static_cast<uint32_t>(a.in_pitch));
+    bytes[cc] = cc < ncs ? (end - start[cc]) * 4u : 0u;
+    total += bytes[cc];
   }
   mbar_arrive_expect_tx(&p.full[slot], total);
   bulk_g2s(p.recs + slot * a.cps * a.rec_bytes, rsrc, ncs * a.rec_bytes, &p.full[slot]);
@@ -145,6 +164,29 @@ __device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, ui
                a.in + static_cast<uint64_t>(ch0 + cc) * a.in_pitch + start[cc], bytes[cc],
                &p.full[slot]);
   }
+}
+
+// The producer lane: issue every chunk as soon as its slot is handed back.
+__device__ __forceinline__ void pipe_produce(const TiledArgs& a, const Pipe& p) {
+  ChunkSpans next = pipe_spans(a, p, 0);
+  for (uint32_t g = 0; g < p.total; ++g) {
+    const ChunkSpans cur = next;
+    if (g + 1 < p.total) next = pipe_spans(a, p, g + 1);
+    const uint32_t use = g / a.nstage;
+    if (use > 0) mbar_wait_sleep(&p.empty[g % a.nstage], (use - 1) & 1u);
+    pipe_issue(a, p, g, cur);
+  }
+}
+
+__device__ __forceinline__ void pipe_init(const TiledArgs& a, const Pipe& p, uint32_t consumers) {
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < a.nstage; ++s) {
+      mbar_init(&p.full[s], 1);
+      mbar_init(&p.empty[s], consumers);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
 }
 
 // Warp-specialised pipeline.  The LAST warp of the CTA is the producer: one
@@ -168,13 +210,7 @@ __device__ __forceinline__ void staged_loop(const TiledArgs& a, uint8_t* smem) {
   }
   __syncthreads();
   if (tid >= consumers * 32) {  // producer warp
-    if (tid == consumers * 32) {
-      for (uint32_t g = 0; g < p.total; ++g) {
-        const uint32_t use = g / a.nstage;
-        if (use > 0) mbar_wait(&p.empty[g % a.nstage], (use - 1) & 1u);
-        pipe_issue(a, p, g);
-      }
-    }
+    if (tid == consumers * 32) pipe_produce(a, p);
     return;
   }
   // Consumer threads beyond the config's items (the block is rounded up to
@@ -239,7 +275,8 @@ struct SmemBody {
     for (int k = 0; k < K; ++k) {
       float* o = a.out + static_cast<uint64_t>(dm0 + id + k * a.items_dm) * a.out_pitch + t0 + it;
 #pragma unroll
-      for (int j = 0; j < W; ++j) o[j * a.items_time] = acc[k][j];
+      for (int j = 0; j < W; ++j)
+        if (t0 + it + j * a.items_time < a.s) o[j * a.items_time] = acc[k][j];
     }
   }
 };
@@ -270,36 +307,124 @@ __global__ void __launch_bounds__(smem_max_threads<K, W>() + 32) k_smem(const Ti
 // bound.  A warp whose K DMs spread further than SPAN in some channel takes
 // the direct per-element path for that channel (any table stays exact).
 // ---------------------------------------------------------------------
-// Five IEEE fp32 adds acc[k][j..j+4] += win[r+j..r+j+4] as one asm block.
-// The case number is baked into the asm text: otherwise the compiler
-// "sinks" the identical add sequences of all cases into one shared block
-// fed by register MOVs (25 MOVs + a compare chain per DM), which is exactly
-// the overhead the jump table exists to avoid.
-#define DDB_ADD5(R, J)                                                              \
-  asm volatile(                                                                     \
-      "add.rn.f32 %0, %0, %5;\n\tadd.rn.f32 %1, %1, %6;\n\tadd.rn.f32 %2, %2, %7;\n\t" \
-      "add.rn.f32 %3, %3, %8;\n\tadd.rn.f32 %4, %4, %9; // rw" #R                   \
-      : "+f"(acc[k][J]), "+f"(acc[k][J + 1]), "+f"(acc[k][J + 2]), "+f"(acc[k][J + 3]), \
-        "+f"(acc[k][J + 4])                                                         \
-      : "f"(win[R + J]), "f"(win[R + J + 1]), "f"(win[R + J + 2]), "f"(win[R + J + 3]), \
-        "f"(win[R + J + 4]))
+// The register-window dispatch (acc[j] += win[rel + j], rel warp-uniform
+// but data-dependent) is generated PTX: one brx.idx.uni jump table per DM
+// (regwin_dispatch.cuh, from gen_dispatch.py).  Written as a C++ switch,
+// nvcc sinks the identical add blocks of all cases into one block fed by
+// register MOVs, or lowers the switch to a compare tree with reconvergence
+// barriers -- both several times the cost of the adds themselves.
+__device__ __forceinline__ float4 lds128(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
 
-#define DDB_CASE(R)                                        \
-  case R:                                                  \
-    if constexpr (R <= SPAN) {                             \
-      _Pragma("unroll") for (int j = 0; j < W; j += 5)     \
-          DDB_ADD5(R, j);                                  \
-    }                                                      \
-    break;
+// Window geometry of a register-window variant.  W % 4 == 0 ("vector"):
+// lanes own W contiguous samples at a stride of W floats with W/4 odd, so
+// 16-byte loads of 32 lanes hit 8 distinct bank groups (conflict-free); the
+// window is read from the 16-byte-aligned address at or below its start and
+// the misalignment (0..3) is folded into every DM's dispatch offset.
+// Otherwise ("scalar", W odd): 4-byte loads at an odd stride, also
+// conflict-free, and DM 0 needs no dispatch.
+template <int W, int SPAN>
+struct RwGeom {
+  static constexpr bool kVec = W % 4 == 0;
+  static constexpr int kMaxRel = kVec ? SPAN + 3 : SPAN;
+  static constexpr int kWin = kVec ? ((W + SPAN + 3 + 3) / 4) * 4 : W + SPAN;
+};
+
+// One staged channel as seen by a register-window warp: its offsets, the
+// fast/slow decision, and (fast) the lane's window in registers.
+template <int K, int W, int SPAN>
+struct RwChan {
+  const float* base;  // lane's column at window position 0 (input time t0+lo)
+  uint32_t off[K];
+  uint32_t al;        // vector mode: misalignment of the window start
+  bool fast;
+  float win[RwGeom<W, SPAN>::kWin];
+};
 
 template <int K, int W, int SPAN>
+struct RegWin {
+  static constexpr int kMaxRel = RwGeom<W, SPAN>::kMaxRel;
+  static constexpr int kWin = RwGeom<W, SPAN>::kWin;
+  static_assert(kMaxRel <= 31, "jump table covers 0..31");
+  static_assert(W % 5 == 0 || W % 4 == 0, "cases add in groups of four or five");
+  float acc[K][W];
+
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int j = 0; j < W; ++j) acc[k][j] = 0.0f;
+  }
+
+  // Issue the shared-memory reads of one channel (results land while the
+  // previous channel's adds run).  The window starts at the warp's FIRST
+  // DM; for non-decreasing rows (every table build_delay_table makes) the
+  // other DMs sit 0..SPAN samples later.  Rows below the first or further
+  // than SPAN take the direct path, so any table stays exact.
+  __device__ __forceinline__ static void load(RwChan<K, W, SPAN>& c, const uint32_t* r,
+                                              const float* w, uint32_t col, uint32_t dml) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) c.off[k] = r[4 + dml + k];
+    bool fast = true;
+#pragma unroll
+    for (int k = 1; k < K; ++k) fast = fast && (c.off[k] - c.off[0] <= static_cast<uint32_t>(SPAN));
+    c.fast = fast;
+    c.base = w + col;
+    if (fast) {
+      const float* p = c.base + c.off[0];
+      if constexpr (RwGeom<W, SPAN>::kVec) {
+        c.al = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p) >> 2) & 3u;
+        const float* pa = p - c.al;
+#pragma unroll
+        for (int i = 0; i < kWin / 4; ++i) {
+          const float4 v = lds128(pa + 4 * i);
+          c.win[4 * i] = v.x;
+          c.win[4 * i + 1] = v.y;
+          c.win[4 * i + 2] = v.z;
+          c.win[4 * i + 3] = v.w;
+        }
+      } else {
+        c.al = 0;
+#pragma unroll
+        for (int i = 0; i < kWin; ++i) c.win[i] = p[i];
+      }
+    }
+  }
+
+  __device__ __forceinline__ void compute(const RwChan<K, W, SPAN>& c) {
+    if (c.fast) {
+      if constexpr (RwGeom<W, SPAN>::kVec) {
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          rw_dispatch<W, kWin, kMaxRel>(acc[k], c.win, c.al + c.off[k] - c.off[0]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < W; ++j) acc[0][j] += c.win[j];
+#pragma unroll
+        for (int k = 1; k < K; ++k) rw_dispatch<W, kWin, kMaxRel>(acc[k], c.win, c.off[k] - c.off[0]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const float* q = c.base + c.off[k];
+#pragma unroll
+        for (int j = 0; j < W; ++j) acc[k][j] += q[j];
+      }
+    }
+  }
+};
+
+// K4 body: one register-window channel at a time (load then compute).  A
+// software-pipelined variant that prefetched the next channel's window was
+// measured 2x slower: the doubled register footprint halved the resident
+// warps, and warp-level parallelism hides the shared-memory latency better.
+template <int K, int W, int SPAN>
 struct RegWinBody {
-  static_assert(SPAN <= 31, "jump table covers 0..31");
-  static_assert(W % 5 == 0, "cases add in groups of five");
   const TiledArgs& a;
   uint32_t col;  // first sample of this lane relative to t0
   uint32_t dml;  // first DM of this warp relative to dm0
-  float acc[K][W];
+  RegWin<K, W, SPAN> rw;
 
   __device__ RegWinBody(const TiledArgs& args) : a(args) {
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -307,66 +432,33 @@ struct RegWinBody {
     col = ((warp % warps_time) * 32 + lane) * W;
     dml = (warp / warps_time) * K;
   }
-  __device__ __forceinline__ void zero() {
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-#pragma unroll
-      for (int j = 0; j < W; ++j) acc[k][j] = 0.0f;
-  }
+  __device__ __forceinline__ void zero() { rw.zero(); }
   __device__ __forceinline__ void channel(const uint32_t* r, const float* w) {
-    uint32_t off[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) off[k] = r[4 + dml + k];
-    // The window starts at the warp's FIRST DM, so for non-decreasing rows
-    // (every table build_delay_table makes) DM 0 reads window[0..W) with no
-    // dispatch; any row below it or further than SPAN takes the direct path.
-    bool fast = true;
-#pragma unroll
-    for (int k = 1; k < K; ++k) fast = fast && (off[k] - off[0] <= static_cast<uint32_t>(SPAN));
-    const float* p = w + col;
-    if (fast) {
-      float win[W + SPAN];
-      p += off[0];
-#pragma unroll
-      for (int i = 0; i < W + SPAN; ++i) win[i] = p[i];
-#pragma unroll
-      for (int j = 0; j < W; ++j) acc[0][j] += win[j];
-#pragma unroll
-      for (int k = 1; k < K; ++k) {
-        switch (off[k] - off[0]) {
-          DDB_CASE(0) DDB_CASE(1) DDB_CASE(2) DDB_CASE(3) DDB_CASE(4) DDB_CASE(5) DDB_CASE(6)
-          DDB_CASE(7) DDB_CASE(8) DDB_CASE(9) DDB_CASE(10) DDB_CASE(11) DDB_CASE(12)
-          DDB_CASE(13) DDB_CASE(14) DDB_CASE(15) DDB_CASE(16) DDB_CASE(17) DDB_CASE(18)
-          DDB_CASE(19) DDB_CASE(20) DDB_CASE(21) DDB_CASE(22) DDB_CASE(23) DDB_CASE(24)
-          DDB_CASE(25) DDB_CASE(26) DDB_CASE(27) DDB_CASE(28) DDB_CASE(29) DDB_CASE(30)
-          DDB_CASE(31)
-          default:
-            break;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const float* q = p + off[k];
-#pragma unroll
-        for (int j = 0; j < W; ++j) acc[k][j] += q[j];
-      }
-    }
+    RwChan<K, W, SPAN> c;
+    RegWin<K, W, SPAN>::load(c, r, w, col, dml);
+    rw.compute(c);
   }
   __device__ __forceinline__ void store(uint32_t dm0, uint32_t t0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       float* o = a.out + static_cast<uint64_t>(dm0 + dml + k) * a.out_pitch + t0 + col;
 #pragma unroll
-      for (int j = 0; j < W; ++j) o[j] = acc[k][j];
+      for (int j = 0; j < W; ++j)
+        if (t0 + col + j < a.s) o[j] = rw.acc[k][j];
     }
   }
 };
-#undef DDB_CASE
-#undef DDB_ADD5
+
+// Register cap per variant: the accumulators, one window and ~40 registers
+// of addressing.  A tight cap is what lets several CTAs share an SM; ptxas
+// left to itself spends the whole file on one CTA.
+template <int K, int W, int SPAN>
+constexpr int regwin_maxreg() {
+  return ((K * W + RwGeom<W, SPAN>::kWin + 40 + 7) / 8) * 8;
+}
 
 template <int K, int W, int SPAN>
-__global__ void __launch_bounds__(288) k_regwin(const TiledArgs a) {
+__global__ void __maxnreg__((regwin_maxreg<K, W, SPAN>())) k_regwin(const TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   staged_loop<RegWinBody<K, W, SPAN>>(a, smem);
 }
@@ -407,8 +499,12 @@ struct RegWinVariant {
 
 #define DDB_R(K, W, S) {K, W, S, k_regwin<K, W, S>}
 static const RegWinVariant kRegWinVariants[] = {
-    DDB_R(2, 25, 8),  DDB_R(2, 25, 16), DDB_R(4, 25, 8),  DDB_R(4, 25, 16), DDB_R(4, 25, 31),
-    DDB_R(4, 5, 8),   DDB_R(4, 5, 16),  DDB_R(8, 5, 16),  DDB_R(8, 5, 31),  DDB_R(16, 5, 31),
+    // scalar windows (W odd: the reference-divisible Apertif/LOFAR shapes)
+    DDB_R(2, 25, 4),  DDB_R(2, 25, 8),  DDB_R(2, 25, 16), DDB_R(4, 25, 12), DDB_R(4, 25, 16),
+    DDB_R(8, 5, 31),
+    // vector windows (W % 4 == 0, W/4 odd; GPU tiling)
+    DDB_R(2, 20, 4),  DDB_R(2, 20, 8),  DDB_R(4, 20, 12), DDB_R(4, 20, 16), DDB_R(4, 12, 12),
+    DDB_R(4, 12, 16), DDB_R(8, 12, 24), DDB_R(8, 12, 28), DDB_R(2, 12, 8),
 };
 #undef DDB_R
 

@@ -28,6 +28,7 @@ struct dd_plan {
   ddb::TiledArgs args{};
   const uint32_t* d_shifts = nullptr;
   uint8_t* d_rec = nullptr;
+  uint2* d_ls = nullptr;
   void (*smem_fn)(const ddb::TiledArgs) = nullptr;
   uint32_t blocks = 0, threads = 0, smem = 0;
   uint32_t grid_y = 1;
@@ -46,7 +47,7 @@ void clear_error();
 cudaError_t launch_delay_table(uint32_t* d_shifts, uint32_t* d_max, uint32_t num_dms,
                                uint32_t channels, uint32_t dm_offset, double f_min, double width,
                                double dm_first, double dm_step, double rate, cudaStream_t st);
-cudaError_t launch_plan(const uint32_t* d_shifts, uint8_t* d_rec, uint32_t* d_max_span,
+cudaError_t launch_plan(const uint32_t* d_shifts, uint8_t* d_rec, uint2* d_ls, uint32_t* d_max_span,
                         unsigned long long* d_span_sum, uint32_t channels, uint32_t tiles_dm,
                         uint32_t tile_dm, uint32_t group, uint32_t rec_bytes, cudaStream_t st);
 cudaError_t launch_max_u32(const uint32_t* d_v, uint64_t n, uint32_t* d_out, cudaStream_t st);

@@ -47,7 +47,7 @@ __global__ void k_delay_table(uint32_t* __restrict__ shifts, uint32_t* __restric
 // max_span[0] = widest tile span; max_span[1] = widest spread of any aligned
 // group of `group` consecutive DMs (the register-window kernel's warp rows).
 __global__ void k_plan(const uint32_t* __restrict__ shifts, uint8_t* __restrict__ rec,
-                       uint32_t* __restrict__ max_span, unsigned long long* __restrict__ span_sum,
+                       uint2* __restrict__ ls, uint32_t* __restrict__ max_span, unsigned long long* __restrict__ span_sum,
                        uint32_t channels, uint32_t tiles_dm, uint32_t tile_dm, uint32_t group,
                        uint32_t rec_bytes) {
   const uint64_t n = static_cast<uint64_t>(tiles_dm) * channels;
@@ -69,6 +69,7 @@ __global__ void k_plan(const uint32_t* __restrict__ shifts, uint8_t* __restrict_
     r[1] = span;
     r[2] = 0;
     r[3] = 0;
+    ls[i] = make_uint2(lo, span);  // compact copy for the staging producer
     for (uint32_t g0 = 0; g0 < tile_dm; g0 += group) {
       uint32_t glo = 0xffffffffu, ghi = 0;
       for (uint32_t l = g0; l < g0 + group && l < tile_dm; ++l) {
@@ -121,13 +122,13 @@ cudaError_t launch_delay_table(uint32_t* d_shifts, uint32_t* d_max, uint32_t num
   return cudaGetLastError();
 }
 
-cudaError_t launch_plan(const uint32_t* d_shifts, uint8_t* d_rec, uint32_t* d_max_span,
+cudaError_t launch_plan(const uint32_t* d_shifts, uint8_t* d_rec, uint2* d_ls, uint32_t* d_max_span,
                         unsigned long long* d_span_sum, uint32_t channels, uint32_t tiles_dm,
                         uint32_t tile_dm, uint32_t group, uint32_t rec_bytes, cudaStream_t st) {
   const uint64_t n = static_cast<uint64_t>(tiles_dm) * channels;
   const uint32_t threads = 128;
   const uint64_t blocks = (n + threads - 1) / threads;
-  k_plan<<<static_cast<uint32_t>(blocks), threads, 0, st>>>(d_shifts, d_rec, d_max_span,
+  k_plan<<<static_cast<uint32_t>(blocks), threads, 0, st>>>(d_shifts, d_rec, d_ls, d_max_span,
                                                             d_span_sum, channels, tiles_dm, tile_dm,
                                                             group ? group : 1, rec_bytes);
   return cudaGetLastError();

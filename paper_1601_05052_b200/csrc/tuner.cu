@@ -62,11 +62,13 @@ bool preferred(const dd_tuning_record& a, const dd_tuning_record& b) {
   const uint64_t ai = static_cast<uint64_t>(a.config.items_time) * a.config.items_dm;
   const uint64_t bi = static_cast<uint64_t>(b.config.items_time) * b.config.items_dm;
   if (ai != bi) return ai < bi;
-  const uint32_t ka[6] = {a.config.items_time, a.config.items_dm, a.config.work_time,
-                          a.config.work_dm, a.config.dm_tile_depth, a.config.staging};
-  const uint32_t kb[6] = {b.config.items_time, b.config.items_dm, b.config.work_time,
-                          b.config.work_dm, b.config.dm_tile_depth, b.config.staging};
-  return std::lexicographical_compare(ka, ka + 6, kb, kb + 6);
+  const uint32_t ka[7] = {a.config.items_time, a.config.items_dm, a.config.work_time,
+                          a.config.work_dm, a.config.dm_tile_depth, a.config.staging,
+                          a.config.flags};
+  const uint32_t kb[7] = {b.config.items_time, b.config.items_dm, b.config.work_time,
+                          b.config.work_dm, b.config.dm_tile_depth, b.config.staging,
+                          b.config.flags};
+  return std::lexicographical_compare(ka, ka + 7, kb, kb + 7);
 }
 
 // CUDA event resolution (the analogue of clock_resolution_seconds,
@@ -171,21 +173,24 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
     if (!(k.items_time % 32 == 0 || k.items_time == 8 || k.items_time == 16)) continue;
     const uint32_t tiles_dm = num_dms / (k.items_dm * k.work_dm);
     if (regwin_shape_ok(k.work_dm, k.work_time, k.items_time, block)) {
-      for (uint32_t depth : {1u, 2u}) {
-        if (depth > 1 && tiles_dm < depth * 2) continue;
+      for (uint32_t cps : {4u, 8u}) {
         dd_config c = k;
-        c.dm_tile_depth = depth;
+        c.dm_tile_depth = 1;
         c.staging = DD_STAGING_REGWIN;
+        c.flags = cps << DD_CONFIG_CPS_SHIFT;
         v.push_back(c);
       }
     }
     if (block < 64 || !smem_variant_ok(k.work_dm, k.work_time, block)) continue;
-    for (uint32_t depth : {1u, 2u, 4u}) {
+    for (uint32_t depth : {1u, 2u}) {
       if (depth > 1 && tiles_dm < depth * 2) continue;
-      dd_config c = k;
-      c.dm_tile_depth = depth;
-      c.staging = DD_STAGING_SMEM;
-      v.push_back(c);
+      for (uint32_t cps : {4u, 8u}) {
+        dd_config c = k;
+        c.dm_tile_depth = depth;
+        c.staging = DD_STAGING_SMEM;
+        c.flags = cps << DD_CONFIG_CPS_SHIFT;
+        v.push_back(c);
+      }
     }
     dd_config c = k;
     c.dm_tile_depth = 1;
@@ -295,6 +300,10 @@ dd_status dd_tune(dd_context* ctx, const dd_setup* setup, uint32_t num_dms,
     dd_plan* p = nullptr;
     st = dd_plan_create(ctx, static_cast<uint32_t*>(d_sh), c, num_dms, s, t, pitch, &space[i],
                         &opt->limits, &p);
+    if (st == DD_ERR_INVALID_ARGUMENT && opt->space == 0) {
+      st = DD_OK;  // a GPU-space shape this instance cannot stage: not a record
+      continue;
+    }
     if (st != DD_OK) break;
     st = dd_plan_time(p, static_cast<float*>(d_in), static_cast<float*>(d_out), s, 1,
                       opt->repeats, runs.data());

@@ -77,7 +77,8 @@ class ShardedDedisperser:
     """This rank's share of one dedispersion instance on its GPU."""
 
     def __init__(self, setup: api.ObservationSetup, num_dms: int, cfg: api.KernelConfig,
-                 dm_tile_depth: int = 1, staging: str = "auto", device: Optional[int] = None):
+                 dm_tile_depth: int = 1, staging: str = "auto", device: Optional[int] = None,
+                 gpu_tiling: bool = False, stage_channels: int = 0):
         self.rank, self.world = world()
         self.setup, self.num_dms, self.cfg = setup, num_dms, cfg
         self.device = torch.cuda.current_device() if device is None else device
@@ -98,7 +99,8 @@ class ShardedDedisperser:
         self.block = torch.empty((c, self.pitch), dtype=torch.float32, device=self.device)
         self.out = torch.empty((self.count, s), dtype=torch.float32, device=self.device)
         self.plan = self.ctx.plan(self.shifts.data_ptr(), c, self.count, s, self.num_samples,
-                                  self.pitch, cfg, dm_tile_depth, staging)
+                                  self.pitch, cfg, dm_tile_depth, staging,
+                                  gpu_tiling=gpu_tiling, stage_channels=stage_channels)
 
     @property
     def flop(self) -> int:

@@ -83,7 +83,7 @@ APERTIF_CFGS = [
     (K(16, 4, 5, 8), 1, "auto"),
     (K(32, 4, 25, 4), 1, "regwin"),
     (K(32, 8, 5, 8), 1, "regwin"),
-    (K(160, 1, 5, 4), 2, "regwin"),
+    (K(160, 1, 5, 8), 2, "regwin"),
     (K(32, 2, 25, 2), 1, "regwin"),
     (K(32, 1, 5, 16), 1, "regwin"),
 ]

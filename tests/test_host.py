@@ -36,8 +36,8 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layouts_match_header():
     assert C.sizeof(N.dd_setup) == 40
-    assert C.sizeof(N.dd_config) == 24
-    assert C.sizeof(N.dd_tuning_record) == 24 + 32 + 8
+    assert C.sizeof(N.dd_config) == 28
+    assert C.sizeof(N.dd_tuning_record) == 32 + 32 + 8
 
 
 def test_no_device_fails_loudly():

@@ -1,6 +1,9 @@
 """Time a list of configs on one instance (device-resident, CUDA events).
 
     python tools/time_configs.py Apertif 4096 "32,4,25,4,1,regwin" "16,16,10,4,1,smem" ...
+
+Extra fields: "g" requests GPU tiling (tile_time need not divide s),
+"cpsN" pins N channels per pipeline stage.
 """
 import os
 import sys
@@ -27,7 +30,10 @@ def main():
         f = spec.split(",")
         cfg = api.KernelConfig(*map(int, f[:4]))
         try:
-            p = ctx.plan(sh.data_ptr(), c, d, s, t, t, cfg, int(f[4]), f[5])
+            extra = f[6:]
+            p = ctx.plan(sh.data_ptr(), c, d, s, t, t, cfg, int(f[4]), f[5],
+                         gpu_tiling="g" in extra,
+                         stage_channels=next((int(x[3:]) for x in extra if x.startswith("cps")), 0))
         except ValueError as e:
             print(f"{spec:28s} invalid: {e}")
             continue

@@ -29,6 +29,7 @@ def record_json(r: api.TuningRecord) -> dict:
     c = r.config
     return {"items_time": c.items_time, "items_dm": c.items_dm, "work_time": c.work_time,
             "work_dm": c.work_dm, "dm_tile_depth": r.dm_tile_depth, "staging": r.staging,
+            "flags": r.flags, "stage_channels": r.stage_channels,
             "family": r.family, "mean_time": r.mean_time, "gflops": r.gflops,
             "timer_warning": r.timer_warning}
 
@@ -83,16 +84,17 @@ def main():
         b = j["best"]
         print(f"{setup.name} d={d}: {len(res.records)} configs in {dt:.1f}s; best "
               f"({b['items_time']},{b['items_dm']},{b['work_time']},{b['work_dm']}) "
-              f"depth={b['dm_tile_depth']} {b['staging']}: {b['gflops']:.1f} GFLOP/s "
+              f"depth={b['dm_tile_depth']} {b['staging']} cps={b['stage_channels']}: "
+              f"{b['gflops']:.1f} GFLOP/s "
               f"({b['mean_time'] * 1e3:.3f} ms, {b['roofline_frac']:.2f}x HBM roofline); "
               f"snr={res.stats.snr_optimum}", flush=True)
     if len(results) > 1:
         rep = api.best_fixed_config(results)
-        k, depth, staging = rep.config
+        k, depth, staging, flags = rep.config
         summ = {"setup": setup.name, "instances": dms,
                 "best_fixed": {"items_time": k.items_time, "items_dm": k.items_dm,
                                "work_time": k.work_time, "work_dm": k.work_dm,
-                               "dm_tile_depth": depth, "staging": staging},
+                               "dm_tile_depth": depth, "staging": staging, "flags": flags},
                 "fixed_gflops": rep.fixed_gflops, "tuned_gflops": [r.best().gflops for r in results],
                 "speedup_over_fixed": rep.speedup_over_fixed}
         with open(os.path.join(a.out, f"{setup.name.lower()}_summary"
