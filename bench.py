@@ -325,7 +325,8 @@ def run_ours(args):
             with open(tpath) as f:
                 tr = json.load(f)
             key = f"{setup.name}_{d}_" + "_".join(str(x) for x in cfgt)
-            traffic = tr.get(key)
+            ent = tr.get(key)
+            traffic = ent.get("dram_bytes_per_launch") if isinstance(ent, dict) else ent
         cs = clk.summary()
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world_size,
