@@ -373,7 +373,7 @@ dd_status dd_validate_config(const dd_config* k, uint32_t num_dms, uint32_t s,
   if (static_cast<uint64_t>(k->work_time) * k->work_dm > L.max_accumulators)
     return fail(DD_ERR_INVALID_ARGUMENT, "work_time * work_dm exceeds the accumulator limit of " +
                                              std::to_string(L.max_accumulators));
-  if (k->staging > DD_STAGING_REGWIN) return fail(DD_ERR_INVALID_ARGUMENT, "unknown staging mode");
+  if (k->staging > DD_STAGING_TMEM) return fail(DD_ERR_INVALID_ARGUMENT, "unknown staging mode");
   if (k->flags & ~(DD_CONFIG_GPU_TILING | DD_CONFIG_CPS_MASK))
     return fail(DD_ERR_INVALID_ARGUMENT, "unknown config flags");
   if (((k->flags & DD_CONFIG_CPS_MASK) >> DD_CONFIG_CPS_SHIFT) > 8)
@@ -502,7 +502,14 @@ dd_status dd_config_family(dd_context* c, const dd_config* k, uint32_t channels,
   }
   switch (k->staging) {
     case DD_STAGING_AUTO:
-      *family = regwin_ok ? DD_STAGING_REGWIN : smem_ok ? DD_STAGING_SMEM : DD_STAGING_DIRECT;
+      *family = smem_ok ? DD_STAGING_SMEM : regwin_ok ? DD_STAGING_REGWIN : DD_STAGING_DIRECT;
+      return DD_OK;
+    case DD_STAGING_TMEM:
+      if (!tmem_shape_ok(k->work_dm, k->work_time, k->items_time, block))
+        return fail(DD_ERR_INVALID_ARGUMENT,
+                    "staging=tmem: needs items_time % 32 == 0, <= 256 threads and an "
+                    "instantiated work_dm x work_time variant");
+      *family = DD_STAGING_TMEM;
       return DD_OK;
     case DD_STAGING_REGWIN:
       if (!regwin_ok)
@@ -579,11 +586,13 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
   const uint64_t block = static_cast<uint64_t>(k->items_time) * k->items_dm;
   const bool smem_shape = smem_variant_ok(k->work_dm, k->work_time, block);
   const bool regwin_shape = regwin_shape_ok(k->work_dm, k->work_time, k->items_time, block);
+  const bool tmem_shape = tmem_shape_ok(k->work_dm, k->work_time, k->items_time, block);
   bool staged = in_pitch % 4 == 0;
   switch (k->staging) {
     case DD_STAGING_AUTO: staged = staged && (smem_shape || regwin_shape); break;
     case DD_STAGING_SMEM: staged = staged && smem_shape; break;
     case DD_STAGING_REGWIN: staged = staged && regwin_shape; break;
+    case DD_STAGING_TMEM: staged = staged && tmem_shape; break;
     default: staged = false;
   }
 
@@ -613,18 +622,19 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
     uint64_t span_sum = 0;
     std::memcpy(&span_sum, scratch + 2, 8);
 
-    // AUTO: register windows when every warp group fits a jump table,
-    // otherwise the shared-memory kernel.
     uint32_t family = k->staging;
     if (family == DD_STAGING_AUTO)
-      family = regwin_shape && p->group_span <= 31 ? DD_STAGING_REGWIN
-               : smem_shape                         ? DD_STAGING_SMEM
-                                                    : DD_STAGING_REGWIN;
+      // AUTO: the shared-memory kernel (fastest measured family, round 1),
+    // register windows where it has no variant.
+    family = smem_shape ? DD_STAGING_SMEM : DD_STAGING_REGWIN;
     ddb::KernelFn fn = nullptr;
     uint32_t slack = 0;
     if (family == DD_STAGING_REGWIN) {
       fn = find_regwin_kernel(k->work_dm, k->work_time, p->group_span, &p->regwin_span);
       slack = p->regwin_span + 4;
+    } else if (family == DD_STAGING_TMEM) {
+      fn = find_tmem_kernel(k->work_dm, k->work_time, p->group_span, &p->regwin_span);
+      slack = p->regwin_span + 8;
     } else {
       fn = find_smem_kernel(k->work_dm, k->work_time);
     }
@@ -670,10 +680,13 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
     p->d_ls = nullptr;
   }
   if (k->staging == DD_STAGING_SMEM || k->staging == DD_STAGING_REGWIN ||
+      k->staging == DD_STAGING_TMEM ||
       (k->flags & DD_CONFIG_GPU_TILING && s % a.tile_time != 0)) {
     delete p;
     return fail(DD_ERR_INVALID_ARGUMENT,
-                std::string("staging=") + (k->staging == DD_STAGING_SMEM ? "smem" : "regwin") +
+                std::string("staging=") +
+                    (k->staging == DD_STAGING_SMEM ? "smem"
+                     : k->staging == DD_STAGING_TMEM ? "tmem" : "regwin") +
                     ": no staged kernel for this config (work_dm x work_time variant, block "
                     "size, items_time, input pitch or shared-memory window)");
   }
@@ -742,7 +755,8 @@ dd_status dd_plan_execute(dd_plan* p, const float* d_in, float* d_out, uint64_t 
   a.in = d_in;
   a.out = d_out;
   a.out_pitch = out_pitch;
-  if (p->family == DD_STAGING_SMEM || p->family == DD_STAGING_REGWIN) {
+  if (p->family == DD_STAGING_SMEM || p->family == DD_STAGING_REGWIN ||
+      p->family == DD_STAGING_TMEM) {
     if ((reinterpret_cast<uintptr_t>(d_in) & 15u) != 0)
       return fail(DD_ERR_INVALID_ARGUMENT, "staged kernels need a 16-byte aligned input");
     DD_CUDA(launch_smem(p->smem_fn, a, p->blocks, p->threads, p->smem, c->stream));

@@ -196,8 +196,9 @@ __device__ __forceinline__ void pipe_init(const TiledArgs& a, const Pipe& p, uin
 // per staged channel, store(dm0, t0) per finished tile; each consumer warp
 // releases a slot with one mbarrier arrival -- there is no CTA-wide barrier
 // in the loop, so warps drift up to nstage stages apart.
-template <class Body>
-__device__ __forceinline__ void staged_loop(const TiledArgs& a, uint8_t* smem) {
+template <class Body, class... Extra>
+__device__ __forceinline__ void staged_loop_with(const TiledArgs& a, uint8_t* smem,
+                                                 Extra... extra) {
   const Pipe p = pipe_setup(a, smem);
   const uint32_t tid = threadIdx.x;
   const uint32_t consumers = blockDim.x / 32 - 1;
@@ -216,7 +217,7 @@ __device__ __forceinline__ void staged_loop(const TiledArgs& a, uint8_t* smem) {
   // Consumer threads beyond the config's items (the block is rounded up to
   // whole warps) only take part in the slot hand-back.
   const bool active = tid < a.items_time * a.items_dm;
-  Body body(a);
+  Body body(a, extra...);
   for (uint32_t g = 0; g < p.total; ++g) {
     const uint32_t q = g % p.nchunk;
     if (q == 0) body.zero();
@@ -236,6 +237,11 @@ __device__ __forceinline__ void staged_loop(const TiledArgs& a, uint8_t* smem) {
     if (active && q == p.nchunk - 1)
       body.store((p.b_first + g / p.nchunk) * a.tile_dm, p.t0);
   }
+}
+
+template <class Body>
+__device__ __forceinline__ void staged_loop(const TiledArgs& a, uint8_t* smem) {
+  staged_loop_with<Body>(a, smem);
 }
 
 // ---------------------------------------------------------------------
@@ -463,6 +469,176 @@ __global__ void __maxnreg__((regwin_maxreg<K, W, SPAN>())) k_regwin(const TiledA
   staged_loop<RegWinBody<K, W, SPAN>>(a, smem);
 }
 
+// ---------------------------------------------------------------------
+// K5: TMEM windows.  Same ownership as K4 (a warp owns K consecutive DMs
+// and 32*W consecutive samples; W % 4 == 0 with W/4 odd so 16-byte window
+// loads are conflict-free), but the data-dependent selection is done by
+// the tensor-memory datapath instead of a jump table: each lane writes its
+// window into its own TMEM row (tcgen05.st, 32x32b), and every DM reads W
+// columns back at the warp-uniform dynamic column offset rel_k
+// (tcgen05.ld at taddr + rel_k) -- TMEM used as a dynamically indexed
+// register file.  The loaded vectors are adjacent registers, so the adds
+// issue as FADD2 (add.rn.f32x2: two independent IEEE RN adds).  Bit-exact:
+// every output still gets one add per channel, channels ascending.
+// ---------------------------------------------------------------------
+template <int N>
+struct TmemShape;
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31, %32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
+      "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]),
+      "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]),
+      "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
+                 "=f"(r[6]), "=f"(r[7])
+               : "r"(taddr)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3])
+               : "r"(taddr)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int K, int W, int SPAN>
+struct TmemBody {
+  static_assert(W % 4 == 0 && (W / 4) % 2 == 1, "W/4 odd: conflict-free 16-byte loads");
+  static_assert(W + SPAN + 3 <= 32, "one 32-column TMEM window per warp");
+  static constexpr int kNV = (W + SPAN + 3 + 3) / 4;  // 16-byte loads per window
+  const TiledArgs& a;
+  uint32_t col, dml, taddr;
+  float acc[K][W];
+
+  __device__ TmemBody(const TiledArgs& args, uint32_t tmem_base) : a(args) {
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t warps_time = a.items_time >> 5;
+    col = ((warp % warps_time) * 32 + lane) * W;
+    dml = (warp / warps_time) * K;
+    // lanes (warp % 4) * 32.. are this warp's TMEM rows; 32 columns per warp
+    taddr = tmem_base + (((warp & 3) * 32) << 16) + (warp >> 2) * 32;
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int j = 0; j < W; ++j) acc[k][j] = 0.0f;
+  }
+  __device__ __forceinline__ void channel(const uint32_t* r, const float* w) {
+    uint32_t off[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) off[k] = r[4 + dml + k];
+    bool fast = true;
+#pragma unroll
+    for (int k = 1; k < K; ++k) fast = fast && (off[k] - off[0] <= static_cast<uint32_t>(SPAN));
+    const float* base = w + col;
+    if (fast) {
+      const float* p = base + off[0];
+      const uint32_t al = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p) >> 2) & 3u;
+      const float* pa = p - al;
+      float win[32];
+#pragma unroll
+      for (int i = 0; i < kNV; ++i) {
+        const float4 v = lds128(pa + 4 * i);
+        win[4 * i] = v.x;
+        win[4 * i + 1] = v.y;
+        win[4 * i + 2] = v.z;
+        win[4 * i + 3] = v.w;
+      }
+#pragma unroll
+      for (int i = 4 * kNV; i < 32; ++i) win[i] = 0.0f;
+      tmem_st32(taddr, win);
+      tmem_wait_st();
+      float v[K][W];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t c = taddr + al + off[k] - off[0];
+#pragma unroll
+        for (int j = 0; j + 8 <= W; j += 8) tmem_ld8(c + j, &v[k][j]);
+        if constexpr (W % 8 == 4) tmem_ld4(c + (W - 4), &v[k][W - 4]);
+      }
+      tmem_wait_ld();
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int j = 0; j < W; j += 2) {
+          const float2 s2 = fadd2(make_float2(acc[k][j], acc[k][j + 1]),
+                                  make_float2(v[k][j], v[k][j + 1]));
+          acc[k][j] = s2.x;
+          acc[k][j + 1] = s2.y;
+        }
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const float* q = base + off[k];
+#pragma unroll
+        for (int j = 0; j < W; ++j) acc[k][j] += q[j];
+      }
+    }
+  }
+  __device__ __forceinline__ void store(uint32_t dm0, uint32_t t0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      float* o = a.out + static_cast<uint64_t>(dm0 + dml + k) * a.out_pitch + t0 + col;
+#pragma unroll
+      for (int j = 0; j < W; ++j)
+        if (t0 + col + j < a.s) o[j] = acc[k][j];
+    }
+  }
+};
+
+// TMEM columns per CTA: 32 per consumer warp beyond the 4 lane quarters,
+// rounded to the allocator's power of two (>= 32).
+__device__ __forceinline__ uint32_t tmem_cols_for(uint32_t consumer_warps) {
+  const uint32_t need = ((consumer_warps + 3) / 4) * 32;
+  uint32_t cols = 32;
+  while (cols < need) cols <<= 1;
+  return cols;
+}
+
+template <int K, int W, int SPAN>
+__global__ void __launch_bounds__(288) k_tmemwin(const TiledArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint32_t tmem_base;
+  const uint32_t consumers = blockDim.x / 32 - 1;
+  const uint32_t cols = tmem_cols_for(consumers);
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_addr(&tmem_base)),
+                 "r"(cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  staged_loop_with<TmemBody<K, W, SPAN>>(a, smem, tmem_base);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (threadIdx.x < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(cols)
+                 : "memory");
+}
+
 // ------------------------------------------------------------ dispatch --
 using KernelFn = void (*)(const TiledArgs);
 
@@ -524,6 +700,40 @@ KernelFn find_regwin_kernel(uint32_t k, uint32_t w, uint32_t group_span, uint32_
   if (pick == nullptr) return nullptr;
   if (span_out) *span_out = static_cast<uint32_t>(pick->span);
   return pick->fn;
+}
+
+struct TmemVariant {
+  int k, w, span;
+  KernelFn fn;
+};
+
+#define DDB_T(K, W, S) {K, W, S, k_tmemwin<K, W, S>}
+static const TmemVariant kTmemVariants[] = {
+    DDB_T(2, 12, 8), DDB_T(4, 12, 12), DDB_T(4, 12, 16), DDB_T(8, 12, 16), DDB_T(2, 20, 8),
+    DDB_T(4, 20, 8),
+};
+#undef DDB_T
+
+KernelFn find_tmem_kernel(uint32_t k, uint32_t w, uint32_t group_span, uint32_t* span_out) {
+  const TmemVariant* cover = nullptr;
+  const TmemVariant* widest = nullptr;
+  for (const TmemVariant& v : kTmemVariants) {
+    if (static_cast<uint32_t>(v.k) != k || static_cast<uint32_t>(v.w) != w) continue;
+    if (widest == nullptr || v.span > widest->span) widest = &v;
+    if (static_cast<uint32_t>(v.span) >= group_span && (cover == nullptr || v.span < cover->span))
+      cover = &v;
+  }
+  const TmemVariant* pick = cover ? cover : widest;
+  if (pick == nullptr) return nullptr;
+  if (span_out) *span_out = static_cast<uint32_t>(pick->span);
+  return pick->fn;
+}
+
+bool tmem_shape_ok(uint32_t k, uint32_t w, uint32_t items_time, uint64_t block) {
+  if (items_time % 32 != 0 || block > 256) return false;
+  for (const TmemVariant& v : kTmemVariants)
+    if (static_cast<uint32_t>(v.k) == k && static_cast<uint32_t>(v.w) == w) return true;
+  return false;
 }
 
 bool regwin_shape_ok(uint32_t k, uint32_t w, uint32_t items_time, uint64_t block) {

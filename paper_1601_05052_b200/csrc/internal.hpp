@@ -60,6 +60,8 @@ KernelFn find_smem_kernel(uint32_t k, uint32_t w, uint32_t* max_threads = nullpt
 // (or the widest one); *span_out = its SPAN.  nullptr when not instantiated.
 KernelFn find_regwin_kernel(uint32_t k, uint32_t w, uint32_t group_span, uint32_t* span_out);
 bool regwin_shape_ok(uint32_t k, uint32_t w, uint32_t items_time, uint64_t block);
+KernelFn find_tmem_kernel(uint32_t k, uint32_t w, uint32_t group_span, uint32_t* span_out);
+bool tmem_shape_ok(uint32_t k, uint32_t w, uint32_t items_time, uint64_t block);
 // True when the staged family can run cfg (block size within the variant's cap).
 inline bool smem_variant_ok(uint32_t k, uint32_t w, uint64_t block) {
   uint32_t cap = 0;

@@ -197,6 +197,30 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
     c.staging = DD_STAGING_DIRECT;
     v.push_back(c);
   }
+  // GPU-native shapes (DD_CONFIG_GPU_TILING, predicated last time tile) for
+  // the window families whose W/4-odd vector loads never divide s exactly
+  // (e.g. 32 x 12 samples per warp): register windows and TMEM windows.
+  for (uint32_t it : {32u, 64u, 128u})
+    for (uint32_t idm : {1u, 2u, 4u, 8u})
+      for (uint32_t wt : {12u, 20u})
+        for (uint32_t wd : {2u, 4u, 8u}) {
+          const uint64_t block = static_cast<uint64_t>(it) * idm;
+          if (block > 256 || num_dms % (idm * wd) != 0 || it * wt >= s * 2u) continue;
+          if (s % (it * wt) == 0) continue;  // already in the reference space
+          dd_config c{it, idm, wt, wd, 1, DD_STAGING_REGWIN, DD_CONFIG_GPU_TILING};
+          if (tmem_shape_ok(wd, wt, it, block)) {
+            for (uint32_t cps : {4u, 8u}) {
+              c.staging = DD_STAGING_TMEM;
+              c.flags = DD_CONFIG_GPU_TILING | (cps << DD_CONFIG_CPS_SHIFT);
+              v.push_back(c);
+            }
+          }
+          if (regwin_shape_ok(wd, wt, it, block)) {
+            c.staging = DD_STAGING_REGWIN;
+            c.flags = DD_CONFIG_GPU_TILING | (4u << DD_CONFIG_CPS_SHIFT);
+            v.push_back(c);
+          }
+        }
   *count = v.size();
   for (uint64_t i = 0; i < v.size() && i < capacity; ++i) out[i] = v[i];
   return DD_OK;

@@ -98,6 +98,8 @@ class ShardedDedisperser:
                                               dm_offset=self.offset)
         self.block = torch.empty((c, self.pitch), dtype=torch.float32, device=self.device)
         self.out = torch.empty((self.count, s), dtype=torch.float32, device=self.device)
+        self._depth, self._staging, self._gpu_tiling, self._cps = (dm_tile_depth, staging,
+                                                                   gpu_tiling, stage_channels)
         self.plan = self.ctx.plan(self.shifts.data_ptr(), c, self.count, s, self.num_samples,
                                   self.pitch, cfg, dm_tile_depth, staging,
                                   gpu_tiling=gpu_tiling, stage_channels=stage_channels)
@@ -119,6 +121,37 @@ class ShardedDedisperser:
         """One pass of this rank's DM range, enqueued on self.stream."""
         self.plan.execute(self.block.data_ptr(), self.out.data_ptr())
         return self.out
+
+    def pipeline(self, chunks: int) -> None:
+        """Prepare run_host(): the shard's DM range cut into `chunks` plans
+        (tile-aligned), each over its slice of the shift table, so the D2H
+        of chunk i overlaps the kernel of chunk i+1."""
+        c, s, td = self.setup.channels, self.setup.samples_per_second, self.cfg.tile_dm()
+        units = self.count // td
+        chunks = max(1, min(chunks, units))
+        self.chunks = []
+        for i in range(chunks):
+            lo = (units * i // chunks) * td
+            hi = (units * (i + 1) // chunks) * td
+            plan = self.ctx.plan(self.shifts.data_ptr() + lo * c * 4, c, hi - lo, s,
+                                 self.num_samples, self.pitch, self.cfg, self._depth,
+                                 self._staging, gpu_tiling=self._gpu_tiling,
+                                 stage_channels=self._cps)
+            self.chunks.append((lo, hi, plan, torch.cuda.Event()))
+        self.copy_stream = torch.cuda.Stream(self.device)
+
+    def run_host(self, host_block: Optional[torch.Tensor], host_out: torch.Tensor) -> None:
+        """End to end from host memory: H2D (+ broadcast) of the block, then
+        per DM chunk: kernel on self.stream, D2H of the chunk's rows on a
+        copy stream once its kernel is done.  host_out: pinned [count][s]."""
+        self.load(host_block)
+        for lo, hi, plan, ev in self.chunks:
+            plan.execute(self.block.data_ptr(), self.out[lo].data_ptr())
+            ev.record(self.stream)
+            with torch.cuda.stream(self.copy_stream):
+                self.copy_stream.wait_event(ev)
+                host_out[lo:hi].copy_(self.out[lo:hi], non_blocking=True)
+        self.copy_stream.synchronize()
 
     def gather(self) -> Optional[torch.Tensor]:
         with torch.cuda.stream(self.stream):

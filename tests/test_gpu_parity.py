@@ -223,6 +223,17 @@ def test_non_monotone_and_fault_injected_tables(dev, golden):
     for cfg in (K(32, 1, 5, 8), K(32, 2, 5, 8), K(32, 4, 5, 8)):
         out = api.dedisperse_tiled(fb2, table2, cfg, api.ExecOptions(staging="regwin"))
         assert np.array_equal(_bits(out.data), _bits(ref2)), cfg
+    # TMEM windows with the same jittered table (GPU tiling: 384 does not divide 320*k)
+    import torch
+    x = torch.from_numpy(fb2.data).cuda()
+    shd = torch.from_numpy(sh2.view(np.int32)).cuda()
+    outd = torch.empty((d, 320), device="cuda")
+    torch.cuda.synchronize()
+    for cfg in (K(32, 2, 12, 4), K(32, 1, 12, 8), K(32, 4, 12, 2)):
+        p = dev.plan(shd.data_ptr(), 24, d, 320, t2, t2, cfg, 1, "tmem", gpu_tiling=True)
+        p.execute(x.data_ptr(), outd.data_ptr())
+        dev.synchronize()
+        assert np.array_equal(_bits(outd.cpu().numpy()), _bits(ref2)), cfg
     # dedisp_tune.cpp:278-287 analogue: one corrupted entry must change the output
     g = golden["baseline"][0]
     setup, table, fb = _golden_instance(g)
@@ -235,7 +246,9 @@ def test_non_monotone_and_fault_injected_tables(dev, golden):
 
 @pytest.mark.parametrize("spec", [
     ("regwin", K(32, 4, 20, 2), 8), ("regwin", K(32, 4, 12, 4), 4), ("regwin", K(32, 2, 12, 8), 8),
-    ("regwin", K(64, 2, 20, 4), 4), ("smem", K(32, 4, 4, 4), 8), ("smem", K(96, 2, 1, 8), 2)])
+    ("regwin", K(64, 2, 20, 4), 4), ("smem", K(32, 4, 4, 4), 8), ("smem", K(96, 2, 1, 8), 2),
+    ("tmem", K(32, 4, 12, 4), 8), ("tmem", K(32, 8, 12, 4), 4), ("tmem", K(64, 2, 12, 2), 8),
+    ("tmem", K(32, 4, 20, 2), 8), ("tmem", K(32, 4, 12, 8), 4), ("tmem", K(32, 8, 20, 4), 8)])
 def test_gpu_tiling_predicated_tail(dev, golden, spec):
     """GPU-native tiles whose tile_time does not divide s (vector register
     windows, odd smem tiles): the predicated last tile must not change a bit."""
@@ -340,3 +353,23 @@ def test_tuner_on_device(dev):
     assert res.realtime_threshold_gflops == pytest.approx(64 * 20000 * 1024 / 1e9)
     z = api.zero_dm_experiment(api.LOFAR, 8, repeats=1, max_configs=4)
     assert z.zero_dm and len(z.records) == 4
+
+
+def test_sharded_driver_host_pipeline(dev, golden):
+    """multi.ShardedDedisperser end to end from pinned host memory with the
+    DM-chunk pipeline (kernel of chunk i+1 overlapping D2H of chunk i)."""
+    import torch
+    from paper_1601_05052_b200 import multi
+    g = golden["baseline"][0]
+    setup, table, fb = _golden_instance(g)
+    dd = multi.ShardedDedisperser(setup, g["num_dms"], K(16, 8, 10, 4), 1, "smem", device=0,
+                                  stage_channels=8)
+    dd.pipeline(3)
+    host = torch.from_numpy(fb.data).pin_memory()
+    out = torch.empty((dd.count, setup.samples_per_second), dtype=torch.float32).pin_memory()
+    dd.run_host(host, out)
+    torch.cuda.synchronize()
+    assert O.fnv1a(out.numpy()) == g["out_fnv"]
+    dd.run()
+    torch.cuda.synchronize()
+    assert O.fnv1a(dd.out.cpu().numpy()) == g["out_fnv"]
