@@ -28,7 +28,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "dedispersion GFLOP/s + HBM GB/s (Apertif/LOFAR, 2-4096 DMs) at 1/2/4/8 B200"
-DEFAULT_CFG = (16, 16, 10, 4, 1, "smem", 8)  # overridden by tuning/<setup>_<d>.json
+DEFAULT_CFG = (16, 8, 10, 4, 1, "smem", 8 << 8)  # overridden by tuning/<setup>_<d>.json
 REASON_FIELDS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
 
@@ -41,7 +41,7 @@ def parse():
     p.add_argument("--setup", default="Apertif")
     p.add_argument("--dms", type=int, default=4096)
     p.add_argument("--config", default=None,
-                   help="items_time,items_dm,work_time,work_dm,depth,staging[,stage_channels]")
+                   help="items_time,items_dm,work_time,work_dm,depth,staging[,flags]")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -65,7 +65,7 @@ def tuned_config(setup_name, d):
         with open(path) as f:
             b = json.load(f)["best"]
         return (b["items_time"], b["items_dm"], b["work_time"], b["work_dm"],
-                b["dm_tile_depth"], b["staging"], b.get("stage_channels", 0)), path
+                b["dm_tile_depth"], b["staging"], b.get("flags", 0)), path
     return DEFAULT_CFG, None
 
 
@@ -228,12 +228,13 @@ def run_ours(args):
     if args.config:
         f = args.config.split(",")
         cfgt, cfg_src = (int(f[0]), int(f[1]), int(f[2]), int(f[3]), int(f[4]), f[5],
-                         int(f[6]) if len(f) > 6 else 0), "cli"
+                         int(f[6], 0) if len(f) > 6 else 0), "cli"
     else:
         cfgt, cfg_src = tuned_config(setup.name, d)
     cfg = api.KernelConfig(*cfgt[:4])
+    flags = cfgt[6]
     dd = multi.ShardedDedisperser(setup, d, cfg, cfgt[4], cfgt[5], device=local,
-                                  stage_channels=cfgt[6])
+                                  gpu_tiling=bool(flags & 1), stage_channels=(flags >> 8) & 15)
     c, s, t = setup.channels, setup.samples_per_second, dd.num_samples
     stream = dd.stream
     torch.cuda.set_stream(stream)  # events, flushes and copies share the library's stream
@@ -343,6 +344,7 @@ def run_ours(args):
                                   "work_time": cfgt[2], "work_dm": cfgt[3],
                                   "dm_tile_depth": cfgt[4], "staging": cfgt[5],
                                   "stage_channels": info["channels_per_stage"],
+                                  "gpu_tiling": bool(flags & 1),
                                   "source": os.path.relpath(cfg_src, ROOT)
                                   if cfg_src and cfg_src != "cli" else (cfg_src or "default")},
                 "kernel_family": info["family"], "smem_bytes": info["smem_bytes"],

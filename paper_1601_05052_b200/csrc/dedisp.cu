@@ -519,11 +519,12 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int K, int W, int SPAN>
+template <int K, int W, int SPAN, int COLS>
 struct TmemBody {
   static_assert(W % 4 == 0 && (W / 4) % 2 == 1, "W/4 odd: conflict-free 16-byte loads");
-  static_assert(W + SPAN + 3 <= 32, "one 32-column TMEM window per warp");
-  static constexpr int kNV = (W + SPAN + 3 + 3) / 4;  // 16-byte loads per window
+  static_assert(COLS == 32 || COLS == 64, "32 or 64 TMEM columns per warp window");
+  static_assert(W + SPAN + 3 <= COLS, "window must fit the warp's TMEM columns");
+  static_assert(K % 2 == 0, "DMs are read back in pairs");
   const TiledArgs& a;
   uint32_t col, dml, taddr;
   float acc[K][W];
@@ -533,8 +534,8 @@ struct TmemBody {
     const uint32_t warps_time = a.items_time >> 5;
     col = ((warp % warps_time) * 32 + lane) * W;
     dml = (warp / warps_time) * K;
-    // lanes (warp % 4) * 32.. are this warp's TMEM rows; 32 columns per warp
-    taddr = tmem_base + (((warp & 3) * 32) << 16) + (warp >> 2) * 32;
+    // lanes (warp % 4) * 32.. are this warp's TMEM rows; COLS columns per warp
+    taddr = tmem_base + (((warp & 3) * 32) << 16) + (warp >> 2) * COLS;
   }
   __device__ __forceinline__ void zero() {
 #pragma unroll
@@ -542,49 +543,65 @@ struct TmemBody {
 #pragma unroll
       for (int j = 0; j < W; ++j) acc[k][j] = 0.0f;
   }
+  // One 32-column half of the window: only the 16-byte vectors the warp's
+  // DMs actually span this channel are read (nv, warp-uniform).
+  __device__ __forceinline__ void stage_half(const float* pa, uint32_t nv, uint32_t tcol) {
+    float win[32];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (static_cast<uint32_t>(i) < nv) v = lds128(pa + 4 * i);
+      win[4 * i] = v.x;
+      win[4 * i + 1] = v.y;
+      win[4 * i + 2] = v.z;
+      win[4 * i + 3] = v.w;
+    }
+    tmem_st32(tcol, win);
+  }
   __device__ __forceinline__ void channel(const uint32_t* r, const float* w) {
     uint32_t off[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) off[k] = r[4 + dml + k];
+    uint32_t spread = 0;
     bool fast = true;
 #pragma unroll
-    for (int k = 1; k < K; ++k) fast = fast && (off[k] - off[0] <= static_cast<uint32_t>(SPAN));
+    for (int k = 1; k < K; ++k) {
+      const uint32_t d = off[k] - off[0];
+      fast = fast && (d <= static_cast<uint32_t>(SPAN));
+      spread = max(spread, d);
+    }
     const float* base = w + col;
     if (fast) {
       const float* p = base + off[0];
       const uint32_t al = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p) >> 2) & 3u;
       const float* pa = p - al;
-      float win[32];
-#pragma unroll
-      for (int i = 0; i < kNV; ++i) {
-        const float4 v = lds128(pa + 4 * i);
-        win[4 * i] = v.x;
-        win[4 * i + 1] = v.y;
-        win[4 * i + 2] = v.z;
-        win[4 * i + 3] = v.w;
+      const uint32_t nv = (al + spread + W + 3) >> 2;  // vectors actually needed
+      stage_half(pa, nv, taddr);
+      if constexpr (COLS == 64) {
+        if (nv > 8) stage_half(pa + 32, nv - 8, taddr + 32);
       }
-#pragma unroll
-      for (int i = 4 * kNV; i < 32; ++i) win[i] = 0.0f;
-      tmem_st32(taddr, win);
       tmem_wait_st();
-      float v[K][W];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const uint32_t c = taddr + al + off[k] - off[0];
+      for (int k = 0; k < K; k += 2) {
+        float v[2][W];
 #pragma unroll
-        for (int j = 0; j + 8 <= W; j += 8) tmem_ld8(c + j, &v[k][j]);
-        if constexpr (W % 8 == 4) tmem_ld4(c + (W - 4), &v[k][W - 4]);
-      }
-      tmem_wait_ld();
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t c = taddr + al + off[k + h] - off[0];
 #pragma unroll
-      for (int k = 0; k < K; ++k)
-#pragma unroll
-        for (int j = 0; j < W; j += 2) {
-          const float2 s2 = fadd2(make_float2(acc[k][j], acc[k][j + 1]),
-                                  make_float2(v[k][j], v[k][j + 1]));
-          acc[k][j] = s2.x;
-          acc[k][j + 1] = s2.y;
+          for (int j = 0; j + 8 <= W; j += 8) tmem_ld8(c + j, &v[h][j]);
+          if constexpr (W % 8 == 4) tmem_ld4(c + (W - 4), &v[h][W - 4]);
         }
+        tmem_wait_ld();
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int j = 0; j < W; j += 2) {
+            const float2 s2 = fadd2(make_float2(acc[k + h][j], acc[k + h][j + 1]),
+                                    make_float2(v[h][j], v[h][j + 1]));
+            acc[k + h][j] = s2.x;
+            acc[k + h][j + 1] = s2.y;
+          }
+      }
     } else {
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -605,21 +622,21 @@ struct TmemBody {
   }
 };
 
-// TMEM columns per CTA: 32 per consumer warp beyond the 4 lane quarters,
-// rounded to the allocator's power of two (>= 32).
-__device__ __forceinline__ uint32_t tmem_cols_for(uint32_t consumer_warps) {
-  const uint32_t need = ((consumer_warps + 3) / 4) * 32;
+// TMEM columns per CTA: `cols` per consumer warp beyond the 4 lane
+// quarters, rounded to the allocator's power of two (>= 32).
+__device__ __forceinline__ uint32_t tmem_cols_for(uint32_t consumer_warps, uint32_t per_warp) {
+  const uint32_t need = ((consumer_warps + 3) / 4) * per_warp;
   uint32_t cols = 32;
   while (cols < need) cols <<= 1;
   return cols;
 }
 
-template <int K, int W, int SPAN>
+template <int K, int W, int SPAN, int COLS>
 __global__ void __launch_bounds__(288) k_tmemwin(const TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint32_t tmem_base;
   const uint32_t consumers = blockDim.x / 32 - 1;
-  const uint32_t cols = tmem_cols_for(consumers);
+  const uint32_t cols = tmem_cols_for(consumers, COLS);
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_addr(&tmem_base)),
@@ -630,7 +647,7 @@ __global__ void __launch_bounds__(288) k_tmemwin(const TiledArgs a) {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  staged_loop_with<TmemBody<K, W, SPAN>>(a, smem, tmem_base);
+  staged_loop_with<TmemBody<K, W, SPAN, COLS>>(a, smem, tmem_base);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -707,10 +724,10 @@ struct TmemVariant {
   KernelFn fn;
 };
 
-#define DDB_T(K, W, S) {K, W, S, k_tmemwin<K, W, S>}
+#define DDB_T(K, W, S, C) {K, W, S, k_tmemwin<K, W, S, C>}
 static const TmemVariant kTmemVariants[] = {
-    DDB_T(2, 12, 8), DDB_T(4, 12, 12), DDB_T(4, 12, 16), DDB_T(8, 12, 16), DDB_T(2, 20, 8),
-    DDB_T(4, 20, 8),
+    DDB_T(2, 12, 8, 32),  DDB_T(4, 12, 12, 32), DDB_T(4, 12, 16, 32), DDB_T(8, 12, 16, 32),
+    DDB_T(8, 12, 32, 64), DDB_T(2, 20, 8, 32),  DDB_T(4, 20, 8, 32),  DDB_T(4, 20, 24, 64),
 };
 #undef DDB_T
 
