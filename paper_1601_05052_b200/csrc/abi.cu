@@ -432,12 +432,13 @@ constexpr uint32_t kSmemBudget = 112 * 1024;  // aim for 2 CTAs per SM
 // Staged-family geometry for a config: shared-memory slots, stage count.
 // `slack` floats per window: the register-window kernel reads up to SPAN
 // samples past a window (never added), which must stay inside the slot.
-bool smem_geometry(const dd_context* c, uint32_t tile_time, uint32_t tile_dm, uint32_t channels,
-                   uint32_t max_span, uint32_t slack, uint32_t want_cps, uint32_t* win_cap,
+bool smem_geometry(const dd_context* c, uint32_t tile_time, uint32_t tile_dm, uint32_t group,
+                   uint32_t channels, uint32_t max_span, uint32_t slack, uint32_t want_cps,
+                   uint32_t* win_cap,
                    uint32_t* rec_bytes, uint32_t* cps, uint32_t* nstage, uint32_t* smem) {
   const uint64_t wc =
       (static_cast<uint64_t>(max_span) + tile_time + slack + 6u + 3u) & ~3ull;
-  const uint64_t rb = ddb::plan_rec_bytes(tile_dm);
+  const uint64_t rb = ddb::plan_rec_bytes(tile_dm, std::max<uint32_t>(1, group));
   const uint64_t slot = rb + 4 * wc;
   const uint64_t limit = static_cast<uint64_t>(c->smem_optin);
   // Prefer 3 stages of several channels within the 2-CTA budget; degrade
@@ -496,7 +497,7 @@ dd_status dd_config_family(dd_context* c, const dd_config* k, uint32_t channels,
   const bool regwin_ok = regwin_shape_ok(k->work_dm, k->work_time, k->items_time, block);
   if (smem_ok) {
     uint32_t a, b, cc, d, e;
-    smem_ok = smem_geometry(c, tile_time, tile_dm, channels, max_span, 0,
+    smem_ok = smem_geometry(c, tile_time, tile_dm, k->work_dm, channels, max_span, 0,
                             (k->flags & DD_CONFIG_CPS_MASK) >> DD_CONFIG_CPS_SHIFT, &a, &b,
                             &cc, &d, &e);
   }
@@ -597,7 +598,7 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
   }
 
   if (staged) {
-    a.rec_bytes = ddb::plan_rec_bytes(a.tile_dm);
+    a.rec_bytes = ddb::plan_rec_bytes(a.tile_dm, k->work_dm);
     const uint64_t rec_total = static_cast<uint64_t>(a.tiles_dm) * channels * a.rec_bytes;
     cudaError_t e = cudaMalloc(&p->d_rec, rec_total);
     if (e == cudaSuccess)
@@ -646,7 +647,7 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
                           static_cast<uint32_t>(fattr.maxThreadsPerBlock) < threads))
       fn = nullptr;
     if (fn != nullptr &&
-        smem_geometry(c, a.tile_time, a.tile_dm, channels, p->max_span, slack,
+        smem_geometry(c, a.tile_time, a.tile_dm, k->work_dm, channels, p->max_span, slack,
                       (k->flags & DD_CONFIG_CPS_MASK) >> DD_CONFIG_CPS_SHIFT, &win_cap,
                       &rec_bytes, &cps, &nstage, &smem)) {
       a.win_cap = win_cap;

@@ -46,6 +46,17 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// 16-byte shared load under a predicate; the destination keeps its old
+// contents when the predicate is off (no zero-fill instructions).
+__device__ __forceinline__ void lds128_if(bool pred, const float* addr, float& x, float& y,
+                                          float& z, float& w) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "@q ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n\t}"
+      : "+f"(x), "+f"(y), "+f"(z), "+f"(w)
+      : "r"(smem_addr(addr)), "r"(static_cast<int>(pred)));
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
@@ -106,8 +117,12 @@ struct PlanRec {
   uint32_t pad0, pad1;
 };
 
-__host__ __device__ inline uint32_t plan_rec_bytes(uint32_t tile_dm) {
-  return ((16u + 4u * tile_dm) + 15u) & ~15u;
+// ... followed by one u32 per aligned group of `group` DMs: the spread of
+// the group's offsets above its FIRST DM (0xffffffff when a later DM sits
+// below it) -- the register/TMEM-window kernels' fast-path test, precomputed.
+__host__ __device__ inline uint32_t plan_rec_bytes(uint32_t tile_dm, uint32_t group = 1) {
+  const uint32_t groups = (tile_dm + group - 1) / group;
+  return ((16u + 4u * tile_dm + 4u * groups) + 15u) & ~15u;
 }
 
 struct TiledArgs {

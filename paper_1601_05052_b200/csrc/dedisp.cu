@@ -543,44 +543,52 @@ struct TmemBody {
 #pragma unroll
       for (int j = 0; j < W; ++j) acc[k][j] = 0.0f;
   }
-  // One 32-column half of the window: only the 16-byte vectors the warp's
-  // DMs actually span this channel are read (nv, warp-uniform).
-  __device__ __forceinline__ void stage_half(const float* pa, uint32_t nv, uint32_t tcol) {
-    float win[32];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (static_cast<uint32_t>(i) < nv) v = lds128(pa + 4 * i);
-      win[4 * i] = v.x;
-      win[4 * i + 1] = v.y;
-      win[4 * i + 2] = v.z;
-      win[4 * i + 3] = v.w;
-    }
-    tmem_st32(tcol, win);
-  }
-  __device__ __forceinline__ void channel(const uint32_t* r, const float* w) {
+  // Per-channel state fetched from shared memory one channel ahead.
+  struct Pre {
     uint32_t off[K];
+    uint32_t spread, al, nv;
+    const float* base;
+    float win[32];  // first 32 window columns (fast path)
+  };
+
+  // Offsets + (fast) the first half of the window: only the 16-byte vectors
+  // the warp's DMs actually span this channel (nv, warp-uniform) are read.
+  __device__ __forceinline__ void fetch(Pre& n, const uint32_t* r, const float* w) const {
 #pragma unroll
-    for (int k = 0; k < K; ++k) off[k] = r[4 + dml + k];
-    uint32_t spread = 0;
-    bool fast = true;
+    for (int k = 0; k < K; ++k) n.off[k] = r[4 + dml + k];
+    n.spread = r[4 + a.tile_dm + dml / K];  // precomputed by k_plan
+    n.base = w + col;
+    const float* p = n.base + n.off[0];
+    n.al = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p) >> 2) & 3u;
+    n.nv = n.spread <= static_cast<uint32_t>(SPAN) ? (n.al + n.spread + W + 3) >> 2 : 0u;
+    const float* pa = p - n.al;
 #pragma unroll
-    for (int k = 1; k < K; ++k) {
-      const uint32_t d = off[k] - off[0];
-      fast = fast && (d <= static_cast<uint32_t>(SPAN));
-      spread = max(spread, d);
-    }
-    const float* base = w + col;
-    if (fast) {
-      const float* p = base + off[0];
-      const uint32_t al = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p) >> 2) & 3u;
-      const float* pa = p - al;
-      const uint32_t nv = (al + spread + W + 3) >> 2;  // vectors actually needed
-      stage_half(pa, nv, taddr);
-      if constexpr (COLS == 64) {
-        if (nv > 8) stage_half(pa + 32, nv - 8, taddr + 32);
+    for (int i = 0; i < 8; ++i)
+      lds128_if(static_cast<uint32_t>(i) < n.nv, pa + 4 * i, n.win[4 * i], n.win[4 * i + 1],
+                n.win[4 * i + 2], n.win[4 * i + 3]);
+  }
+
+  // Window -> this lane's TMEM row; afterwards n.win may be refilled.
+  __device__ __forceinline__ void commit(const Pre& n) const {
+    if (n.nv == 0) return;
+    tmem_st32(taddr, n.win);
+    if constexpr (COLS == 64) {
+      if (n.nv > 8) {
+        const float* pa = n.base + n.off[0] - n.al + 32;
+        float hi[32];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          lds128_if(static_cast<uint32_t>(i) < n.nv - 8, pa + 4 * i, hi[4 * i], hi[4 * i + 1],
+                    hi[4 * i + 2], hi[4 * i + 3]);
+        tmem_st32(taddr + 32, hi);
       }
-      tmem_wait_st();
+    }
+    tmem_wait_st();
+  }
+
+  __device__ __forceinline__ void accumulate(const uint32_t (&off)[K], uint32_t al, bool fast,
+                                             const float* base) {
+    if (fast) {
 #pragma unroll
       for (int k = 0; k < K; k += 2) {
         float v[2][W];
@@ -610,6 +618,39 @@ struct TmemBody {
         for (int j = 0; j < W; ++j) acc[k][j] += q[j];
       }
     }
+  }
+
+  // A stage's channels, software pipelined one channel deep: the next
+  // channel's offsets and window are read from shared memory while this
+  // channel's TMEM reads and adds issue.
+  __device__ __forceinline__ void chunk(const uint8_t* rbase, const float* wbase, uint32_t ncs,
+                                        uint32_t t0) {
+    Pre n;
+    {
+      const uint32_t* r = reinterpret_cast<const uint32_t*>(rbase);
+      fetch(n, r, wbase + ((t0 + r[0]) & 3u));
+    }
+    for (uint32_t cc = 0; cc < ncs; ++cc) {
+      commit(n);
+      uint32_t off[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) off[k] = n.off[k];
+      const uint32_t al = n.al;
+      const bool fast = n.nv != 0;
+      const float* base = n.base;
+      if (cc + 1 < ncs) {
+        const uint32_t* r = reinterpret_cast<const uint32_t*>(rbase + (cc + 1) * a.rec_bytes);
+        fetch(n, r, wbase + (cc + 1) * a.win_cap + ((t0 + r[0]) & 3u));
+      }
+      accumulate(off, al, fast, base);
+    }
+  }
+
+  __device__ __forceinline__ void channel(const uint32_t* r, const float* w) {
+    Pre n;
+    fetch(n, r, w);
+    commit(n);
+    accumulate(n.off, n.al, n.nv != 0, n.base);
   }
   __device__ __forceinline__ void store(uint32_t dm0, uint32_t t0) {
 #pragma unroll

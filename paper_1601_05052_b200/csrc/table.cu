@@ -72,13 +72,17 @@ __global__ void k_plan(const uint32_t* __restrict__ shifts, uint8_t* __restrict_
     ls[i] = make_uint2(lo, span);  // compact copy for the staging producer
     for (uint32_t g0 = 0; g0 < tile_dm; g0 += group) {
       uint32_t glo = 0xffffffffu, ghi = 0;
+      const uint32_t first = col[static_cast<uint64_t>(g0) * channels];
+      bool below = false;
       for (uint32_t l = g0; l < g0 + group && l < tile_dm; ++l) {
         const uint32_t v = col[static_cast<uint64_t>(l) * channels];
         r[4 + l] = v - lo;
         glo = min(glo, v);
         ghi = max(ghi, v);
+        below = below || v < first;
       }
       gspan = max(gspan, ghi - glo);
+      r[4 + tile_dm + g0 / group] = below ? 0xffffffffu : ghi - first;
     }
   }
   const uint32_t sum = __reduce_add_sync(0xffffffffu, span);
