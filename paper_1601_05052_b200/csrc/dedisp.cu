@@ -673,7 +673,7 @@ __device__ __forceinline__ uint32_t tmem_cols_for(uint32_t consumer_warps, uint3
 }
 
 template <int K, int W, int SPAN, int COLS>
-__global__ void __launch_bounds__(288) k_tmemwin(const TiledArgs a) {
+__device__ __forceinline__ void tmemwin_run(const TiledArgs& a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint32_t tmem_base;
   const uint32_t consumers = blockDim.x / 32 - 1;
@@ -695,6 +695,11 @@ __global__ void __launch_bounds__(288) k_tmemwin(const TiledArgs a) {
   if (threadIdx.x < 32)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(cols)
                  : "memory");
+}
+
+template <int K, int W, int SPAN, int COLS>
+__global__ void __launch_bounds__(288) k_tmemwin(const TiledArgs a) {
+  tmemwin_run<K, W, SPAN, COLS>(a);
 }
 
 // ------------------------------------------------------------ dispatch --
