@@ -620,32 +620,11 @@ struct TmemBody {
     }
   }
 
-  // A stage's channels, software pipelined one channel deep: the next
-  // channel's offsets and window are read from shared memory while this
-  // channel's TMEM reads and adds issue.
-  __device__ __forceinline__ void chunk(const uint8_t* rbase, const float* wbase, uint32_t ncs,
-                                        uint32_t t0) {
-    Pre n;
-    {
-      const uint32_t* r = reinterpret_cast<const uint32_t*>(rbase);
-      fetch(n, r, wbase + ((t0 + r[0]) & 3u));
-    }
-    for (uint32_t cc = 0; cc < ncs; ++cc) {
-      commit(n);
-      uint32_t off[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) off[k] = n.off[k];
-      const uint32_t al = n.al;
-      const bool fast = n.nv != 0;
-      const float* base = n.base;
-      if (cc + 1 < ncs) {
-        const uint32_t* r = reinterpret_cast<const uint32_t*>(rbase + (cc + 1) * a.rec_bytes);
-        fetch(n, r, wbase + (cc + 1) * a.win_cap + ((t0 + r[0]) & 3u));
-      }
-      accumulate(off, al, fast, base);
-    }
-  }
-
+  // Per channel: fetch (offsets + window from shared memory), commit
+  // (window -> TMEM), accumulate (TMEM reads + FADD2).  A variant that
+  // software-pipelined fetch(c+1) under accumulate(c) was measured 2x
+  // slower: the extra live window registers spilled at the 168-register
+  // cap that keeps two CTAs per SM.
   __device__ __forceinline__ void channel(const uint32_t* r, const float* w) {
     Pre n;
     fetch(n, r, w);
