@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--flush-mb", type=int, default=256)
     p.add_argument("--e2e-chunks", type=int, default=8)
+    p.add_argument("--e2e-channel-groups", type=int, default=2)
     return p.parse_args()
 
 
@@ -286,7 +287,7 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         h_out = torch.empty((dd.count, s), dtype=torch.float32).pin_memory()
-        dd.pipeline(args.e2e_chunks)
+        dd.pipeline(args.e2e_chunks, args.e2e_channel_groups)
         e2e_ms = []
         for i in range(max(2, args.steps // 3) + 1):
             if world_size > 1:
@@ -305,10 +306,12 @@ def run_ours(args):
                "ms_per_step": round(e2e_ms_v, 3),
                "h2d_bytes_per_step": c * t * 4 if rank == 0 else 0,
                "d2h_bytes_per_step": d * s * 4,
-               "chunks": len(dd.chunks),
-               "path": "pinned H2D of the [c][t] block (rank 0) + NCCL broadcast, then per DM "
-                       "chunk: kernel, and D2H of the chunk's output rows overlapped with the "
-                       "next chunk's kernel; host-timed, synchronised at the end"}
+               "dm_chunks": len(dd.chunks), "channel_groups": len(dd.groups),
+               "path": "pinned H2D of the [c][t] block by channel groups overlapped with the "
+                       "kernels of the groups already landed (accumulating through the output, "
+                       "bit-exact; with N>1: H2D on rank 0 + NCCL broadcast), and D2H of each "
+                       "DM chunk's rows overlapped with the remaining kernels; host-timed, "
+                       "synchronised at the end"}
 
     cpu = None
     if rank == 0 and world_size == 1 and not args.no_cpu:

@@ -204,6 +204,16 @@ dd_status dd_plan_get_info(const dd_plan* plan, dd_plan_info* info);
  * bit-identical to dedisperse_reference for every config. */
 dd_status dd_plan_execute(dd_plan* plan, const float* d_in, float* d_out, uint64_t out_pitch);
 
+/* Staged families only: run channels [ch_begin, ch_end) of the pass.
+ * accumulate = 0 starts every output at 0.0f, 1 continues from the values
+ * already in d_out.  Splitting a pass into ascending channel ranges
+ * (first with accumulate = 0) is bit-identical to one dd_plan_execute -- the
+ * per-output fp32 running sum round-trips through memory exactly -- which
+ * lets the input block stream in by channel ranges under the compute. */
+dd_status dd_plan_execute_channels(dd_plan* plan, const float* d_in, float* d_out,
+                                   uint64_t out_pitch, uint32_t ch_begin, uint32_t ch_end,
+                                   int accumulate);
+
 /* Time `repeats` executions with CUDA events on the context stream after
  * `warmup` untimed ones (benchmark_config, tuner.cpp:136-170).  seconds[i]
  * receives each run. */

@@ -115,6 +115,7 @@ SIGNATURES = {
     "dd_plan_get_info": (i32, [P, C.POINTER(dd_plan_info)]),
     "dd_plan_execute": (i32, [P, P, P, u64]),
     "dd_plan_time": (i32, [P, P, P, u64, u32, u32, pdbl]),
+    "dd_plan_execute_channels": (i32, [P, P, P, u64, u32, u32, C.c_int]),
     "dd_dedisperse_device": (i32, [P, P, u32, u64, u64, P, u32, u32, C.POINTER(dd_config),
                                    C.POINTER(dd_limits), P]),
     "dd_dedisperse": (i32, [P, P, u32, u64, P, u32, u32, C.POINTER(dd_config),

@@ -412,6 +412,13 @@ class Plan:
         check(lib().dd_plan_execute(self.handle, C.c_void_p(d_in), C.c_void_p(d_out),
                                     out_pitch or self.s))
 
+    def execute_channels(self, d_in: int, d_out: int, ch_begin: int, ch_end: int,
+                         accumulate: bool, out_pitch: Optional[int] = None) -> None:
+        """Channels [ch_begin, ch_end) only; accumulate continues from d_out."""
+        check(lib().dd_plan_execute_channels(self.handle, C.c_void_p(d_in), C.c_void_p(d_out),
+                                             out_pitch or self.s, ch_begin, ch_end,
+                                             int(accumulate)))
+
     def time(self, d_in: int, d_out: int, warmup: int = 1, repeats: int = 10,
              out_pitch: Optional[int] = None) -> List[float]:
         runs = (C.c_double * max(repeats, 1))()

@@ -581,6 +581,9 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
   a.tile_dm = k->items_dm * k->work_dm;
   a.tiles_time = (s + a.tile_time - 1) / a.tile_time;  // last tile predicated (GPU tiling)
   a.tiles_dm = num_dms / a.tile_dm;
+  a.ch_begin = 0;
+  a.ch_end = channels;
+  a.accumulate = 0;
   a.depth = std::max<uint32_t>(1, k->dm_tile_depth);
   a.depth = std::min(a.depth, a.tiles_dm);
 
@@ -764,6 +767,31 @@ dd_status dd_plan_execute(dd_plan* p, const float* d_in, float* d_out, uint64_t 
   } else {
     DD_CUDA(launch_direct(a, p->blocks, p->threads, c->stream));
   }
+  return DD_OK;
+}
+
+dd_status dd_plan_execute_channels(dd_plan* p, const float* d_in, float* d_out,
+                                   uint64_t out_pitch, uint32_t ch_begin, uint32_t ch_end,
+                                   int accumulate) {
+  if (p == nullptr || d_in == nullptr || d_out == nullptr)
+    return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  if (p->reference_order || p->family == DD_STAGING_DIRECT)
+    return fail(DD_ERR_INVALID_ARGUMENT, "channel ranges need a staged kernel family");
+  if (ch_begin >= ch_end || ch_end > p->args.channels)
+    return fail(DD_ERR_INVALID_ARGUMENT, "bad channel range");
+  if (out_pitch < p->args.s) return fail(DD_ERR_INVALID_ARGUMENT, "output pitch below s");
+  if ((reinterpret_cast<uintptr_t>(d_in) & 15u) != 0)
+    return fail(DD_ERR_INVALID_ARGUMENT, "staged kernels need a 16-byte aligned input");
+  dd_context* c = p->ctx;
+  DD_CUDA(cudaSetDevice(c->device));
+  ddb::TiledArgs a = p->args;
+  a.in = d_in;
+  a.out = d_out;
+  a.out_pitch = out_pitch;
+  a.ch_begin = ch_begin;
+  a.ch_end = ch_end;
+  a.accumulate = accumulate ? 1u : 0u;
+  DD_CUDA(launch_smem(p->smem_fn, a, p->blocks, p->threads, p->smem, c->stream));
   return DD_OK;
 }
 

@@ -143,6 +143,11 @@ struct TiledArgs {
   uint32_t nstage;
   uint32_t pack;       // tiles per CTA (direct family)
   uint32_t vthreads;   // virtual threads per CTA (direct family)
+  // staged families: channel range of this launch; accumulate = 1 starts
+  // every output from its current value in `out` instead of 0.0f (a pass
+  // split by channel ranges then reproduces the single pass bit for bit:
+  // the running fp32 sum round-trips through memory exactly)
+  uint32_t ch_begin, ch_end, accumulate;
 };
 
 }  // namespace ddb

@@ -112,7 +112,7 @@ __device__ __forceinline__ Pipe pipe_setup(const TiledArgs& a, uint8_t* smem) {
   p.t0 = (blockIdx.x / groups_dm) * a.tile_time;
   p.b_first = (blockIdx.x % groups_dm) * a.depth;
   const uint32_t ntiles = min(a.depth, a.tiles_dm - p.b_first);
-  p.nchunk = (a.channels + a.cps - 1) / a.cps;
+  p.nchunk = (a.ch_end - a.ch_begin + a.cps - 1) / a.cps;
   p.total = ntiles * p.nchunk;
   return p;
 }
@@ -126,8 +126,8 @@ struct ChunkSpans {
 __device__ __forceinline__ ChunkSpans pipe_spans(const TiledArgs& a, const Pipe& p, uint32_t g) {
   ChunkSpans c;
   const uint32_t b = p.b_first + g / p.nchunk;
-  const uint32_t ch0 = (g % p.nchunk) * a.cps;
-  const uint32_t ncs = min(a.cps, a.channels - ch0);
+  const uint32_t ch0 = a.ch_begin + (g % p.nchunk) * a.cps;
+  const uint32_t ncs = min(a.cps, a.ch_end - ch0);
   const uint2* src = a.ls + static_cast<uint64_t>(b) * a.channels + ch0;
 #pragma unroll
   for (uint32_t cc = 0; cc < 8; ++cc) c.v[cc] = cc < ncs ? __ldg(src + cc) : make_uint2(0, 0);
@@ -139,8 +139,8 @@ __device__ __forceinline__ ChunkSpans pipe_spans(const TiledArgs& a, const Pipe&
 __device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, uint32_t g,
                                            const ChunkSpans& cs) {
   const uint32_t b = p.b_first + g / p.nchunk;
-  const uint32_t ch0 = (g % p.nchunk) * a.cps;
-  const uint32_t ncs = min(a.cps, a.channels - ch0);
+  const uint32_t ch0 = a.ch_begin + (g % p.nchunk) * a.cps;
+  const uint32_t ncs = min(a.cps, a.ch_end - ch0);
   const uint32_t slot = g % a.nstage;
   const uint8_t* rsrc = a.rec + (static_cast<uint64_t>(b) * a.channels + ch0) * a.rec_bytes;
   uint32_t start[8], bytes[8];
@@ -220,10 +220,15 @@ __device__ __forceinline__ void staged_loop_with(const TiledArgs& a, uint8_t* sm
   Body body(a, extra...);
   for (uint32_t g = 0; g < p.total; ++g) {
     const uint32_t q = g % p.nchunk;
-    if (q == 0) body.zero();
+    if (q == 0) {
+      if (a.accumulate && active)
+        body.load((p.b_first + g / p.nchunk) * a.tile_dm, p.t0);
+      else
+        body.zero();
+    }
     const uint32_t slot = g % a.nstage;
     mbar_wait(&p.full[slot], (g / a.nstage) & 1u);
-    const uint32_t ncs = min(a.cps, a.channels - q * a.cps);
+    const uint32_t ncs = min(a.cps, a.ch_end - (a.ch_begin + q * a.cps));
     const uint8_t* rbase = p.recs + slot * a.cps * a.rec_bytes;
     const float* wbase = p.wins + static_cast<uint64_t>(slot) * a.cps * a.win_cap;
     if (active) {
@@ -274,6 +279,16 @@ struct SmemBody {
       const float* p = w + r[4 + id + k * a.items_dm];
 #pragma unroll
       for (int j = 0; j < W; ++j) acc[k][j] += p[j * a.items_time];
+    }
+  }
+  __device__ __forceinline__ void load(uint32_t dm0, uint32_t t0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const float* o =
+          a.out + static_cast<uint64_t>(dm0 + id + k * a.items_dm) * a.out_pitch + t0 + it;
+#pragma unroll
+      for (int j = 0; j < W; ++j)
+        acc[k][j] = t0 + it + j * a.items_time < a.s ? o[j * a.items_time] : 0.0f;
     }
   }
   __device__ __forceinline__ void store(uint32_t dm0, uint32_t t0) {
@@ -439,6 +454,14 @@ struct RegWinBody {
     dml = (warp / warps_time) * K;
   }
   __device__ __forceinline__ void zero() { rw.zero(); }
+  __device__ __forceinline__ void load(uint32_t dm0, uint32_t t0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const float* o = a.out + static_cast<uint64_t>(dm0 + dml + k) * a.out_pitch + t0 + col;
+#pragma unroll
+      for (int j = 0; j < W; ++j) rw.acc[k][j] = t0 + col + j < a.s ? o[j] : 0.0f;
+    }
+  }
   __device__ __forceinline__ void channel(const uint32_t* r, const float* w) {
     RwChan<K, W, SPAN> c;
     RegWin<K, W, SPAN>::load(c, r, w, col, dml);
@@ -630,6 +653,14 @@ struct TmemBody {
     fetch(n, r, w);
     commit(n);
     accumulate(n.off, n.al, n.nv != 0, n.base);
+  }
+  __device__ __forceinline__ void load(uint32_t dm0, uint32_t t0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const float* o = a.out + static_cast<uint64_t>(dm0 + dml + k) * a.out_pitch + t0 + col;
+#pragma unroll
+      for (int j = 0; j < W; ++j) acc[k][j] = t0 + col + j < a.s ? o[j] : 0.0f;
+    }
   }
   __device__ __forceinline__ void store(uint32_t dm0, uint32_t t0) {
 #pragma unroll

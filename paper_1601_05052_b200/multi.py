@@ -122,10 +122,13 @@ class ShardedDedisperser:
         self.plan.execute(self.block.data_ptr(), self.out.data_ptr())
         return self.out
 
-    def pipeline(self, chunks: int) -> None:
+    def pipeline(self, chunks: int, channel_groups: int = 4) -> None:
         """Prepare run_host(): the shard's DM range cut into `chunks` plans
-        (tile-aligned), each over its slice of the shift table, so the D2H
-        of chunk i overlaps the kernel of chunk i+1."""
+        (tile-aligned), each over its slice of the shift table, so the D2H of
+        chunk i overlaps the kernel of chunk i+1; and (single rank, staged
+        families) the channel axis cut into `channel_groups` so the H2D of
+        group g+1 overlaps the kernels of group g (accumulating through the
+        output, bit-exact)."""
         c, s, td = self.setup.channels, self.setup.samples_per_second, self.cfg.tile_dm()
         units = self.count // td
         chunks = max(1, min(chunks, units))
@@ -138,19 +141,41 @@ class ShardedDedisperser:
                                  self._staging, gpu_tiling=self._gpu_tiling,
                                  stage_channels=self._cps)
             self.chunks.append((lo, hi, plan, torch.cuda.Event()))
+        staged = self.chunks[0][2].info()["family"] in ("smem", "regwin", "tmem")
+        g = max(1, min(channel_groups, c)) if (staged and self.world == 1) else 1
+        self.groups = [(c * i // g, c * (i + 1) // g, torch.cuda.Event()) for i in range(g)]
+        self.h2d_stream = torch.cuda.Stream(self.device)
         self.copy_stream = torch.cuda.Stream(self.device)
 
     def run_host(self, host_block: Optional[torch.Tensor], host_out: torch.Tensor) -> None:
-        """End to end from host memory: H2D (+ broadcast) of the block, then
-        per DM chunk: kernel on self.stream, D2H of the chunk's rows on a
-        copy stream once its kernel is done.  host_out: pinned [count][s]."""
-        self.load(host_block)
-        for lo, hi, plan, ev in self.chunks:
-            plan.execute(self.block.data_ptr(), self.out[lo].data_ptr())
-            ev.record(self.stream)
-            with torch.cuda.stream(self.copy_stream):
-                self.copy_stream.wait_event(ev)
-                host_out[lo:hi].copy_(self.out[lo:hi], non_blocking=True)
+        """End to end from host memory: the block's channel groups go H2D on
+        their own stream (or, with several ranks, H2D + broadcast); the
+        kernels of channel group g start as soon as its rows landed; each DM
+        chunk's output rows go D2H as soon as its last kernel is done.
+        host_out: pinned [count][s]."""
+        t = self.num_samples
+        if len(self.groups) == 1:
+            self.load(host_block)
+        else:
+            with torch.cuda.stream(self.h2d_stream):
+                for c0, c1, ev in self.groups:
+                    self.block[c0:c1, :t].copy_(host_block[c0:c1], non_blocking=True)
+                    ev.record(self.h2d_stream)
+        last = len(self.groups) - 1
+        for gi, (c0, c1, ev) in enumerate(self.groups):
+            if len(self.groups) > 1:
+                self.stream.wait_event(ev)
+            for lo, hi, plan, done in self.chunks:
+                if len(self.groups) == 1:
+                    plan.execute(self.block.data_ptr(), self.out[lo].data_ptr())
+                else:
+                    plan.execute_channels(self.block.data_ptr(), self.out[lo].data_ptr(), c0, c1,
+                                          accumulate=gi > 0)
+                if gi == last:
+                    done.record(self.stream)
+                    with torch.cuda.stream(self.copy_stream):
+                        self.copy_stream.wait_event(done)
+                        host_out[lo:hi].copy_(self.out[lo:hi], non_blocking=True)
         self.copy_stream.synchronize()
 
     def gather(self) -> Optional[torch.Tensor]:

@@ -364,7 +364,8 @@ def test_sharded_driver_host_pipeline(dev, golden):
     setup, table, fb = _golden_instance(g)
     dd = multi.ShardedDedisperser(setup, g["num_dms"], K(16, 8, 10, 4), 1, "smem", device=0,
                                   stage_channels=8)
-    dd.pipeline(3)
+    dd.pipeline(3, 4)
+    assert len(dd.groups) == 4
     host = torch.from_numpy(fb.data).pin_memory()
     out = torch.empty((dd.count, setup.samples_per_second), dtype=torch.float32).pin_memory()
     dd.run_host(host, out)
@@ -373,3 +374,32 @@ def test_sharded_driver_host_pipeline(dev, golden):
     dd.run()
     torch.cuda.synchronize()
     assert O.fnv1a(dd.out.cpu().numpy()) == g["out_fnv"]
+    # the TMEM family with GPU tiling, same pipeline
+    dd2 = multi.ShardedDedisperser(setup, g["num_dms"], K(32, 4, 12, 8), 1, "tmem", device=0,
+                                   gpu_tiling=True, stage_channels=8)
+    dd2.pipeline(2, 3)
+    out.zero_()
+    dd2.run_host(host, out)
+    torch.cuda.synchronize()
+    assert O.fnv1a(out.numpy()) == g["out_fnv"]
+
+
+@pytest.mark.parametrize("staging,cfg,tiling", [("smem", K(16, 8, 10, 4), False),
+                                                ("tmem", K(32, 4, 12, 8), True),
+                                                ("regwin", K(32, 4, 25, 2), False)])
+def test_channel_range_passes_are_bit_identical(dev, golden, staging, cfg, tiling):
+    """dd_plan_execute_channels: ascending channel ranges accumulating through
+    the output equal one pass bit for bit (the streamed-input e2e path)."""
+    import torch
+    g = golden["baseline"][0]
+    setup, table, fb = _golden_instance(g)
+    d, s, c, t = g["num_dms"], setup.samples_per_second, setup.channels, g["num_samples"]
+    x = torch.from_numpy(fb.data).cuda()
+    sh = torch.from_numpy(table.shifts.view(np.int32)).cuda()
+    out = torch.full((d, s), float("nan"), device="cuda")
+    torch.cuda.synchronize()
+    p = dev.plan(sh.data_ptr(), c, d, s, t, t, cfg, 1, staging, gpu_tiling=tiling)
+    for i, (c0, c1) in enumerate([(0, 100), (100, 101), (101, 640), (640, 1024)]):
+        p.execute_channels(x.data_ptr(), out.data_ptr(), c0, c1, accumulate=i > 0)
+    dev.synchronize()
+    assert O.fnv1a(out.cpu().numpy()) == g["out_fnv"]
