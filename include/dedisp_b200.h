@@ -214,6 +214,14 @@ dd_status dd_plan_execute_channels(dd_plan* plan, const float* d_in, float* d_ou
                                    uint64_t out_pitch, uint32_t ch_begin, uint32_t ch_end,
                                    int accumulate);
 
+/* Staged families only: `beams` independent beams in one launch (grid.y),
+ * beam b reading d_in + b*in_beam_stride (a [channels][in_pitch] block) and
+ * writing d_out + b*out_beam_stride (rows of out_pitch), all with this plan's
+ * shift table -- many beams per device. */
+dd_status dd_plan_execute_beams(dd_plan* plan, uint32_t beams, const float* d_in,
+                                uint64_t in_beam_stride, float* d_out, uint64_t out_pitch,
+                                uint64_t out_beam_stride);
+
 /* Time `repeats` executions with CUDA events on the context stream after
  * `warmup` untimed ones (benchmark_config, tuner.cpp:136-170).  seconds[i]
  * receives each run. */
@@ -236,6 +244,17 @@ dd_status dd_dedisperse(dd_context* ctx, const float* h_in, uint32_t channels,
                         uint64_t num_samples, const uint32_t* h_shifts, uint32_t num_dms,
                         uint32_t samples_per_second, const dd_config* cfg,
                         const dd_limits* limits, float* h_out);
+
+/* ------------------------------------------------ SIGPROC ingest ------ */
+/* Device transpose of a SIGPROC payload (time-major, channel 0 = highest
+ * frequency, float32 [num_samples][channels]) into the channel-major,
+ * lowest-first filterbank layout at d_dst (row pitch dst_pitch floats) --
+ * the transpose of reference sigproc.cpp:177-189.  *first_bad receives the
+ * payload index of the first non-finite sample (the reference raises
+ * format_error at byte offset header_end + 4*index) or -1.  Synchronous. */
+dd_status dd_sigproc_to_filterbank(dd_context* ctx, const float* d_payload, uint32_t channels,
+                                   uint64_t num_samples, float* d_dst, uint64_t dst_pitch,
+                                   int64_t* first_bad);
 
 /* ---------------------------------------------- synthetic input ------- */
 /* noise_filterbank, filterbank.cpp:60-80: mt19937_64(seed), Box-Muller,

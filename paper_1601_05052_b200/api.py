@@ -365,6 +365,18 @@ class Context:
                                           int(zero), C.c_void_p(d_shifts), C.byref(md)))
         return md.value
 
+    def sigproc_to_filterbank(self, d_payload: int, channels: int, num_samples: int,
+                              d_dst: int, dst_pitch: int) -> int:
+        """Device transpose of a SIGPROC payload (time-major, highest channel
+        first) into the channel-major lowest-first layout (reference
+        sigproc.cpp:177-189).  Returns the payload index of the first
+        non-finite sample, or -1."""
+        bad = C.c_int64()
+        check(lib().dd_sigproc_to_filterbank(self.handle, C.c_void_p(d_payload), channels,
+                                             num_samples, C.c_void_p(d_dst), dst_pitch,
+                                             C.byref(bad)))
+        return bad.value
+
     def plan(self, d_shifts: int, channels: int, num_dms: int, samples_per_second: int,
              num_samples: int, in_pitch: int, cfg: Optional[KernelConfig] = None,
              dm_tile_depth: int = 1, staging: str = "auto",
@@ -418,6 +430,13 @@ class Plan:
         check(lib().dd_plan_execute_channels(self.handle, C.c_void_p(d_in), C.c_void_p(d_out),
                                              out_pitch or self.s, ch_begin, ch_end,
                                              int(accumulate)))
+
+    def execute_beams(self, beams: int, d_in: int, in_beam_stride: int, d_out: int,
+                      out_beam_stride: int, out_pitch: Optional[int] = None) -> None:
+        """`beams` independent beams in one launch (strides in floats)."""
+        check(lib().dd_plan_execute_beams(self.handle, beams, C.c_void_p(d_in), in_beam_stride,
+                                          C.c_void_p(d_out), out_pitch or self.s,
+                                          out_beam_stride))
 
     def time(self, d_in: int, d_out: int, warmup: int = 1, repeats: int = 10,
              out_pitch: Optional[int] = None) -> List[float]:

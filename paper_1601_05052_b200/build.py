@@ -19,7 +19,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdedisp_b200.so")
-SOURCES = ["table.cu", "dedisp.cu", "abi.cu", "tuner.cu", "host.cpp"]
+SOURCES = ["table.cu", "dedisp.cu", "abi.cu", "tuner.cu", "ingest.cu", "host.cpp"]
 HEADERS = ["common.cuh", "internal.hpp", "regwin_dispatch.cuh"]
 PUBLIC = [os.path.join(ROOT, "include", "dedisp_b200.h"),
           os.path.join(ROOT, "include", "dedisp", "b200.hpp")]

@@ -584,6 +584,8 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
   a.ch_begin = 0;
   a.ch_end = channels;
   a.accumulate = 0;
+  a.in_beam_stride = 0;
+  a.out_beam_stride = 0;
   a.depth = std::max<uint32_t>(1, k->dm_tile_depth);
   a.depth = std::min(a.depth, a.tiles_dm);
 
@@ -792,6 +794,32 @@ dd_status dd_plan_execute_channels(dd_plan* p, const float* d_in, float* d_out,
   a.ch_end = ch_end;
   a.accumulate = accumulate ? 1u : 0u;
   DD_CUDA(launch_smem(p->smem_fn, a, p->blocks, p->threads, p->smem, c->stream));
+  return DD_OK;
+}
+
+dd_status dd_plan_execute_beams(dd_plan* p, uint32_t beams, const float* d_in,
+                                uint64_t in_beam_stride, float* d_out, uint64_t out_pitch,
+                                uint64_t out_beam_stride) {
+  if (p == nullptr || d_in == nullptr || d_out == nullptr)
+    return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  if (beams == 0 || beams > 65535) return fail(DD_ERR_INVALID_ARGUMENT, "beams must be 1..65535");
+  if (p->reference_order || p->family == DD_STAGING_DIRECT)
+    return fail(DD_ERR_INVALID_ARGUMENT, "beam batching needs a staged kernel family");
+  if (out_pitch < p->args.s) return fail(DD_ERR_INVALID_ARGUMENT, "output pitch below s");
+  if (beams > 1 && (in_beam_stride < p->args.in_pitch * p->args.channels ||
+                    out_beam_stride < out_pitch * p->args.num_dms))
+    return fail(DD_ERR_INVALID_ARGUMENT, "beam strides overlap");
+  if ((reinterpret_cast<uintptr_t>(d_in) & 15u) != 0 || in_beam_stride % 4 != 0)
+    return fail(DD_ERR_INVALID_ARGUMENT, "staged kernels need 16-byte aligned beam inputs");
+  dd_context* c = p->ctx;
+  DD_CUDA(cudaSetDevice(c->device));
+  ddb::TiledArgs a = p->args;
+  a.in = d_in;
+  a.out = d_out;
+  a.out_pitch = out_pitch;
+  a.in_beam_stride = in_beam_stride;
+  a.out_beam_stride = out_beam_stride;
+  DD_CUDA(launch_smem(p->smem_fn, a, p->blocks, p->threads, p->smem, c->stream, beams));
   return DD_OK;
 }
 

@@ -148,6 +148,10 @@ struct TiledArgs {
   // split by channel ranges then reproduces the single pass bit for bit:
   // the running fp32 sum round-trips through memory exactly)
   uint32_t ch_begin, ch_end, accumulate;
+  // staged families: independent beams (grid.y), each with its own input
+  // block and output rows at these strides (floats) -- the deployment's
+  // many-beams-per-GPU batching
+  uint64_t in_beam_stride, out_beam_stride;
 };
 
 }  // namespace ddb

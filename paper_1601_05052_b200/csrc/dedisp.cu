@@ -94,6 +94,11 @@ __global__ void __launch_bounds__(256) k_direct(const TiledArgs a) {
 // DM-fastest so concurrently resident CTAs share one time range and the
 // input is read from HBM about once (the L2 holds the sliding window).
 // ---------------------------------------------------------------------
+// This CTA's beam: output rows of beam blockIdx.y (staged families).
+__device__ __forceinline__ float* beam_out(const TiledArgs& a) {
+  return a.out + blockIdx.y * a.out_beam_stride;
+}
+
 struct Pipe {
   uint64_t* full;   // [nstage] data landed (TMA transaction count)
   uint64_t* empty;  // [nstage] every consumer warp is done with the slot
@@ -161,7 +166,9 @@ __device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, ui
   for (uint32_t cc = 0; cc < 8; ++cc) {
     if (cc < ncs)
       bulk_g2s(p.wins + static_cast<uint64_t>(slot * a.cps + cc) * a.win_cap,
-               a.in + static_cast<uint64_t>(ch0 + cc) * a.in_pitch + start[cc], bytes[cc],
+               a.in + blockIdx.y * a.in_beam_stride + static_cast<uint64_t>(ch0 + cc) * a.in_pitch +
+                   start[cc],
+               bytes[cc],
                &p.full[slot]);
   }
 }
@@ -285,7 +292,7 @@ struct SmemBody {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const float* o =
-          a.out + static_cast<uint64_t>(dm0 + id + k * a.items_dm) * a.out_pitch + t0 + it;
+          beam_out(a) + static_cast<uint64_t>(dm0 + id + k * a.items_dm) * a.out_pitch + t0 + it;
 #pragma unroll
       for (int j = 0; j < W; ++j)
         acc[k][j] = t0 + it + j * a.items_time < a.s ? o[j * a.items_time] : 0.0f;
@@ -294,7 +301,8 @@ struct SmemBody {
   __device__ __forceinline__ void store(uint32_t dm0, uint32_t t0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      float* o = a.out + static_cast<uint64_t>(dm0 + id + k * a.items_dm) * a.out_pitch + t0 + it;
+      float* o =
+          beam_out(a) + static_cast<uint64_t>(dm0 + id + k * a.items_dm) * a.out_pitch + t0 + it;
 #pragma unroll
       for (int j = 0; j < W; ++j)
         if (t0 + it + j * a.items_time < a.s) o[j * a.items_time] = acc[k][j];
@@ -457,7 +465,7 @@ struct RegWinBody {
   __device__ __forceinline__ void load(uint32_t dm0, uint32_t t0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const float* o = a.out + static_cast<uint64_t>(dm0 + dml + k) * a.out_pitch + t0 + col;
+      const float* o = beam_out(a) + static_cast<uint64_t>(dm0 + dml + k) * a.out_pitch + t0 + col;
 #pragma unroll
       for (int j = 0; j < W; ++j) rw.acc[k][j] = t0 + col + j < a.s ? o[j] : 0.0f;
     }
@@ -470,7 +478,7 @@ struct RegWinBody {
   __device__ __forceinline__ void store(uint32_t dm0, uint32_t t0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      float* o = a.out + static_cast<uint64_t>(dm0 + dml + k) * a.out_pitch + t0 + col;
+      float* o = beam_out(a) + static_cast<uint64_t>(dm0 + dml + k) * a.out_pitch + t0 + col;
 #pragma unroll
       for (int j = 0; j < W; ++j)
         if (t0 + col + j < a.s) o[j] = rw.acc[k][j];
@@ -657,7 +665,7 @@ struct TmemBody {
   __device__ __forceinline__ void load(uint32_t dm0, uint32_t t0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const float* o = a.out + static_cast<uint64_t>(dm0 + dml + k) * a.out_pitch + t0 + col;
+      const float* o = beam_out(a) + static_cast<uint64_t>(dm0 + dml + k) * a.out_pitch + t0 + col;
 #pragma unroll
       for (int j = 0; j < W; ++j) acc[k][j] = t0 + col + j < a.s ? o[j] : 0.0f;
     }
@@ -665,7 +673,7 @@ struct TmemBody {
   __device__ __forceinline__ void store(uint32_t dm0, uint32_t t0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      float* o = a.out + static_cast<uint64_t>(dm0 + dml + k) * a.out_pitch + t0 + col;
+      float* o = beam_out(a) + static_cast<uint64_t>(dm0 + dml + k) * a.out_pitch + t0 + col;
 #pragma unroll
       for (int j = 0; j < W; ++j)
         if (t0 + col + j < a.s) o[j] = acc[k][j];
@@ -834,8 +842,8 @@ cudaError_t launch_direct(const TiledArgs& a, uint32_t blocks, uint32_t threads,
 }
 
 cudaError_t launch_smem(KernelFn fn, const TiledArgs& a, uint32_t blocks, uint32_t threads,
-                        uint32_t smem, cudaStream_t st) {
-  fn<<<blocks, threads, smem, st>>>(a);
+                        uint32_t smem, cudaStream_t st, uint32_t beams) {
+  fn<<<dim3(blocks, beams), threads, smem, st>>>(a);
   return cudaGetLastError();
 }
 

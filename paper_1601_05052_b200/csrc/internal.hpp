@@ -73,7 +73,7 @@ cudaError_t launch_reference(const float* in, uint64_t pitch, const uint32_t* sh
 cudaError_t launch_direct(const TiledArgs& a, uint32_t blocks, uint32_t threads,
                           cudaStream_t st);
 cudaError_t launch_smem(KernelFn fn, const TiledArgs& a, uint32_t blocks, uint32_t threads,
-                        uint32_t smem, cudaStream_t st);
+                        uint32_t smem, cudaStream_t st, uint32_t beams = 1);
 cudaError_t prepare_smem(KernelFn fn, uint32_t smem);
 
 // host logic shared with the tuner (abi.cu)

@@ -403,3 +403,76 @@ def test_channel_range_passes_are_bit_identical(dev, golden, staging, cfg, tilin
         p.execute_channels(x.data_ptr(), out.data_ptr(), c0, c1, accumulate=i > 0)
     dev.synchronize()
     assert O.fnv1a(out.cpu().numpy()) == g["out_fnv"]
+
+
+@pytest.mark.parametrize("staging,cfg,tiling", [("smem", K(16, 8, 10, 4), False),
+                                                ("tmem", K(32, 4, 12, 8), True)])
+def test_beam_batching(dev, staging, cfg, tiling):
+    """dd_plan_execute_beams: B independent beams in one launch equal B single
+    passes (each checked against the oracle on a DM subset)."""
+    import torch
+    setup, d, beams = api.APERTIF, 64, 3
+    s, c = setup.samples_per_second, setup.channels
+    t = api.instance_sizing(setup, d).num_samples
+    table = api.build_delay_table(setup, d)
+    blocks = [api.noise_filterbank(setup, t, 1.0, 10 + b).data for b in range(beams)]
+    x = torch.from_numpy(np.stack(blocks)).cuda()
+    sh = torch.from_numpy(table.shifts.view(np.int32)).cuda()
+    out = torch.full((beams, d, s), float("nan"), device="cuda")
+    torch.cuda.synchronize()
+    p = dev.plan(sh.data_ptr(), c, d, s, t, t, cfg, 1, staging, gpu_tiling=tiling)
+    p.execute_beams(beams, x.data_ptr(), c * t, out.data_ptr(), d * s)
+    dev.synchronize()
+    got = out.cpu().numpy()
+    rows = [0, 17, 63]
+    for b in range(beams):
+        ref = O.dedisperse_reference(blocks[b], table.shifts[rows], s)
+        assert np.array_equal(_bits(got[b][rows]), _bits(ref)), b
+
+
+def test_block_stream_matches_one_shot(dev):
+    """stream.BlockStream: consecutive seconds pushed one at a time give, for
+    every full window, exactly the one-shot pass over the same samples."""
+    import torch
+    from paper_1601_05052_b200.stream import BlockStream
+    setup = api.ObservationSetup("strm", 320, 24, 300.0, 1.0, 0.0, 0.5)
+    d = 32
+    st = BlockStream(setup, d, K(32, 2, 5, 8), 1, "smem", device=0)
+    s, t = setup.samples_per_second, st.t
+    total = t + 3 * s
+    series = api.noise_filterbank(setup, total, 1.0, 21).data
+    table = api.build_delay_table(setup, d)
+    outs = []
+    for n in range(total // s):
+        o = st.push(torch.from_numpy(series[:, n * s:(n + 1) * s]).cuda())
+        if o is not None:
+            st.stream.synchronize()
+            outs.append(o.cpu().numpy().copy())
+    assert len(outs) == (total - t) // s + 1
+    for i, o in enumerate(outs):
+        ref = O.dedisperse_reference(np.ascontiguousarray(series[:, i * s:i * s + t]),
+                                     table.shifts, s)
+        assert np.array_equal(_bits(o), _bits(ref)), i
+
+
+def test_sigproc_transpose_on_device(dev):
+    """dd_sigproc_to_filterbank equals the reference's host transpose
+    (sigproc.cpp:177-189: time-major, highest channel first -> channel-major,
+    lowest first) and reports the first non-finite sample."""
+    import torch
+    rng = np.random.default_rng(4)
+    c, t = 37, 1001
+    payload = rng.standard_normal((t, c)).astype(np.float32)
+    expect = payload[:, ::-1].T.copy()
+    src = torch.from_numpy(payload).cuda()
+    pitch = 1004
+    dst = torch.zeros((c, pitch), device="cuda")
+    torch.cuda.synchronize()
+    bad = dev.sigproc_to_filterbank(src.data_ptr(), c, t, dst.data_ptr(), pitch)
+    assert bad == -1
+    assert np.array_equal(dst.cpu().numpy()[:, :t], expect)
+    payload[500, 3] = np.inf
+    payload[700, 1] = np.nan
+    src = torch.from_numpy(payload).cuda()
+    torch.cuda.synchronize()
+    assert dev.sigproc_to_filterbank(src.data_ptr(), c, t, dst.data_ptr(), pitch) == 500 * c + 3

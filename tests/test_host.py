@@ -195,3 +195,17 @@ def test_roofline_definitions():
     assert abs(api.roofline_gflops(4096, 20000, 1024, 6549.8) - 1635.8) < 0.5
     assert math.isclose(api.realtime_threshold_gflops(api.APERTIF, 4096), 83.88608)
     assert api.ai_bounds(4096, 20000, 1024)[0] == 0.25
+
+
+def test_cxx_dropin_header_compiles_and_links(tmp_path):
+    """The C++ drop-in (include/dedisp/b200.hpp) builds like reference client
+    code and links against the library (running it needs a GPU)."""
+    import subprocess
+    exe = str(tmp_path / "dropin")
+    pkg = os.path.join(ROOT, "paper_1601_05052_b200")
+    O.lib()
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cxx", "test_dropin.cpp"), "-L", pkg,
+                        "-ldedisp_b200", "-L", os.path.join(ROOT, "oracle"), "-loracle",
+                        "-o", exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
