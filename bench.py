@@ -61,12 +61,14 @@ def peaks():
 
 
 def tuned_config(setup_name, d):
+    from paper_1601_05052_b200 import api
     path = os.path.join(ROOT, "tuning", f"{setup_name.lower()}_{d}.json")
     if os.path.exists(path):
         with open(path) as f:
-            b = json.load(f)["best"]
-        return (b["items_time"], b["items_dm"], b["work_time"], b["work_dm"],
-                b["dm_tile_depth"], b["staging"], b.get("flags", 0)), path
+            b = api.tuning_result_from_json(f.read()).best()
+        k = b.config
+        return (k.items_time, k.items_dm, k.work_time, k.work_dm, b.dm_tile_depth, b.staging,
+                b.flags), path
     return DEFAULT_CFG, None
 
 

@@ -87,6 +87,10 @@ typedef struct dd_config {
  * reference-compatible entry points (dd_validate_config without the flag,
  * dd_dedisperse) keep the reference's exact-division rule. */
 #define DD_CONFIG_GPU_TILING 0x1u
+/* TMEM windows: use the three-CTAs-per-SM build (<= 128 registers,
+ * <= 4 consumer warps per CTA) when one exists for the shape; otherwise the
+ * flag is ignored.  A tuning knob: occupancy against register pressure. */
+#define DD_CONFIG_HIGH_OCCUPANCY 0x2u
 /* Staged families: channels per pipeline stage in bits 8..11 (1..8; 0 lets
  * the plan choose).  A tuning knob: larger stages amortise the per-stage
  * synchronisation, smaller ones leave shared memory for more CTAs per SM. */
@@ -167,7 +171,9 @@ dd_status dd_validate_config(const dd_config* cfg, uint32_t num_dms,
 dd_status dd_config_family(dd_context* ctx, const dd_config* cfg, uint32_t channels,
                            uint32_t num_dms, uint32_t samples_per_second, uint32_t max_span,
                            uint32_t* family);
-/* count_loads, count_loads.cpp:9-68 (host arithmetic over a host table). */
+/* count_loads, count_loads.cpp:9-68 (host arithmetic over a host table).
+ * With DD_CONFIG_GPU_TILING in cfg->flags the predicated last time tile is
+ * counted like a full tile (what the staging producer copies). */
 dd_status dd_count_loads(const uint32_t* h_shifts, uint32_t channels, uint32_t num_dms,
                          uint32_t samples_per_second, const dd_config* cfg, uint64_t* staged,
                          uint64_t* ideal);
@@ -195,6 +201,8 @@ typedef struct dd_plan_info {
   uint32_t channels_per_stage, stages;
   uint32_t kernel_launches; /* launches per dd_plan_execute */
   uint64_t staged_bytes;  /* L2->SMEM bytes per execute (0 for direct) */
+  uint32_t registers;     /* per thread, of the tiled kernel (0 otherwise) */
+  uint32_t ctas_per_sm;   /* resident CTAs per SM (occupancy API; 0 otherwise) */
 } dd_plan_info;
 dd_status dd_plan_get_info(const dd_plan* plan, dd_plan_info* info);
 

@@ -11,12 +11,13 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libdedisp_b200.so")
+LIB_PATH = os.environ.get("DDB_LIB") or os.path.join(PKG, "libdedisp_b200.so")
 
 DD_OK, DD_ERR_INVALID_ARGUMENT, DD_ERR_CAPACITY, DD_ERR_CUDA, DD_ERR_NO_DEVICE, DD_ERR_INTERNAL = range(6)
 STAGING = {"auto": 0, "smem": 1, "direct": 2, "regwin": 3, "tmem": 4}
 STAGING_NAME = {v: k for k, v in STAGING.items()}
 DD_CONFIG_GPU_TILING = 0x1
+DD_CONFIG_HIGH_OCCUPANCY = 0x2
 DD_CONFIG_CPS_SHIFT = 8
 DD_CONFIG_CPS_MASK = 0xF << DD_CONFIG_CPS_SHIFT
 
@@ -55,7 +56,8 @@ class dd_plan_info(C.Structure):
                 ("grid_x", C.c_uint32), ("grid_y", C.c_uint32), ("block_threads", C.c_uint32),
                 ("smem_bytes", C.c_uint32), ("channels_per_stage", C.c_uint32),
                 ("stages", C.c_uint32), ("kernel_launches", C.c_uint32),
-                ("staged_bytes", C.c_uint64)]
+                ("staged_bytes", C.c_uint64), ("registers", C.c_uint32),
+                ("ctas_per_sm", C.c_uint32)]
 
 
 class dd_tune_options(C.Structure):

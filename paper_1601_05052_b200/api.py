@@ -16,6 +16,7 @@ Device-resident workflows (the bench, the multi-GPU driver) use
 from __future__ import annotations
 
 import ctypes as C
+import json
 import math
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -234,8 +235,11 @@ class LoadCounts:
 
 
 def _cfg(cfg: KernelConfig, depth: int = 1, staging: str = "auto",
-         gpu_tiling: bool = False, stage_channels: int = 0) -> N.dd_config:
-    flags = (N.DD_CONFIG_GPU_TILING if gpu_tiling else 0) | (stage_channels << N.DD_CONFIG_CPS_SHIFT)
+         gpu_tiling: bool = False, stage_channels: int = 0,
+         high_occupancy: bool = False) -> N.dd_config:
+    flags = ((N.DD_CONFIG_GPU_TILING if gpu_tiling else 0)
+             | (N.DD_CONFIG_HIGH_OCCUPANCY if high_occupancy else 0)
+             | (stage_channels << N.DD_CONFIG_CPS_SHIFT))
     return N.dd_config(cfg.items_time, cfg.items_dm, cfg.work_time, cfg.work_dm, depth,
                        N.STAGING[staging], flags)
 
@@ -319,14 +323,17 @@ def dedisperse_tiled(fb: Filterbank, table: DelayTable, cfg: KernelConfig,
 
 
 def count_loads(table: DelayTable, cfg: KernelConfig, num_dms: int,
-                samples_per_second: int) -> LoadCounts:
-    """reference count_loads.cpp:9-68"""
+                samples_per_second: int, flags: int = 0) -> LoadCounts:
+    """reference count_loads.cpp:9-68 (flags: DD_CONFIG_GPU_TILING counts a
+    predicated last time tile like a full one)."""
     if num_dms == 0 or num_dms != table.num_dms:
         raise ValueError("delay table does not cover the requested trial count")
     sh = np.ascontiguousarray(table.shifts, np.uint32)
     st, idl = C.c_uint64(), C.c_uint64()
+    kc = _cfg(cfg)
+    kc.flags = flags
     check(lib().dd_count_loads(sh.ctypes.data, table.setup.channels, num_dms, samples_per_second,
-                               C.byref(_cfg(cfg)), C.byref(st), C.byref(idl)))
+                               C.byref(kc), C.byref(st), C.byref(idl)))
     return LoadCounts(st.value, idl.value)
 
 
@@ -381,22 +388,29 @@ class Context:
              num_samples: int, in_pitch: int, cfg: Optional[KernelConfig] = None,
              dm_tile_depth: int = 1, staging: str = "auto",
              limits: KernelLimits = KernelLimits(), gpu_tiling: bool = False,
-             stage_channels: int = 0) -> "Plan":
+             stage_channels: int = 0, high_occupancy: bool = False, flags: int = 0) -> "Plan":
         """gpu_tiling: tile_time need not divide s (staged families only);
-        stage_channels: channels per pipeline stage (0 = plan's choice)."""
+        stage_channels: channels per pipeline stage (0 = plan's choice);
+        high_occupancy: TMEM windows' three-CTA build; flags: raw DD_CONFIG_*
+        bits OR-ed in (as stored in tuning records)."""
         return Plan(self, d_shifts, channels, num_dms, samples_per_second, num_samples, in_pitch,
-                    cfg, dm_tile_depth, staging, limits, gpu_tiling, stage_channels)
+                    cfg, dm_tile_depth, staging, limits, gpu_tiling, stage_channels,
+                    high_occupancy, flags)
 
 
 class Plan:
     """dd_plan: a table + config bound to one kernel launch."""
 
     def __init__(self, ctx: Context, d_shifts, channels, num_dms, s, num_samples, in_pitch,
-                 cfg, depth, staging, limits, gpu_tiling=False, stage_channels=0):
+                 cfg, depth, staging, limits, gpu_tiling=False, stage_channels=0,
+                 high_occupancy=False, flags=0):
         self.ctx = ctx
         self.num_dms, self.s, self.channels = num_dms, s, channels
         h = C.c_void_p()
-        kc = _cfg(cfg, depth, staging, gpu_tiling, stage_channels) if cfg is not None else None
+        kc = _cfg(cfg, depth, staging, gpu_tiling, stage_channels,
+                  high_occupancy) if cfg is not None else None
+        if kc is not None:
+            kc.flags |= flags
         check(lib().dd_plan_create(ctx.handle, C.c_void_p(d_shifts), channels, num_dms, s,
                                    num_samples, in_pitch, C.byref(kc) if kc is not None else None,
                                    C.byref(limits.c()), C.byref(h)))
@@ -684,3 +698,208 @@ def algorithmic_bytes(num_dms: int, samples_per_second: int, channels: int) -> i
 def roofline_gflops(num_dms: int, samples_per_second: int, channels: int, hbm_gbs: float) -> float:
     d, s, c = num_dms, samples_per_second, channels
     return d * s * c / (algorithmic_bytes(d, s, c) / (hbm_gbs * 1e9)) / 1e9
+
+
+@dataclass(frozen=True)
+class MemoryTraffic:
+    """reference analysis.hpp:26-30 (elements of 4 bytes)."""
+
+    staged_loads: int
+    output_writes: int
+    delay_reads: int
+
+
+def kernel_traffic(table: DelayTable, cfg: KernelConfig, num_dms: int,
+                   samples_per_second: int, flags: int = 0) -> MemoryTraffic:
+    """reference analysis.cpp:23-31: count_loads' staged loads + one write
+    per output + one read per table entry."""
+    loads = count_loads(table, cfg, num_dms, samples_per_second, flags)
+    return MemoryTraffic(loads.staged_loads, num_dms * samples_per_second,
+                         num_dms * table.setup.channels)
+
+
+def measured_ai(flops: int, traffic: MemoryTraffic) -> float:
+    """reference analysis.cpp:33-38"""
+    elements = traffic.staged_loads + traffic.output_writes + traffic.delay_reads
+    if elements == 0:
+        raise ValueError("no memory traffic to divide by")
+    return float(flops) / (4.0 * float(elements))
+
+
+class NotRealTimeError(RuntimeError):
+    """reference errors.hpp not_real_time_error"""
+
+
+@dataclass(frozen=True)
+class DeploymentPlan:
+    beams_per_device: int
+    devices: int
+
+
+def deployment_sizing(setup: ObservationSetup, num_dms: int, beams: int,
+                      measured_time_per_pass: float) -> DeploymentPlan:
+    """reference analysis.cpp:47-65"""
+    setup.validate()
+    if num_dms == 0:
+        raise ValueError("need at least one trial DM")
+    if beams == 0:
+        raise ValueError("need at least one beam")
+    t = measured_time_per_pass
+    if not math.isfinite(t) or t <= 0.0:
+        raise ValueError("pass time must be a positive number of seconds")
+    if t >= 1.0:
+        raise NotRealTimeError(f"one pass takes {t} s; a device cannot keep up with even a "
+                               "single beam")
+    per = int(1.0 / t)
+    return DeploymentPlan(per, (beams + per - 1) // per)
+
+
+@dataclass(frozen=True)
+class RooflineVerdict:
+    memory_bound: bool
+    ridge_flop_per_byte: float
+    attainable_gflops: float
+
+
+def classify_roofline(ai_flop_per_byte: float, peak_gflops: float,
+                      peak_gbs: float) -> RooflineVerdict:
+    """reference analysis.cpp:79-93"""
+    if not math.isfinite(ai_flop_per_byte) or ai_flop_per_byte <= 0.0:
+        raise ValueError("arithmetic intensity must be positive")
+    if (not math.isfinite(peak_gflops) or peak_gflops <= 0.0 or not math.isfinite(peak_gbs)
+            or peak_gbs <= 0.0):
+        raise ValueError("device peaks must be positive")
+    ridge = peak_gflops / peak_gbs
+    return RooflineVerdict(ai_flop_per_byte < ridge, ridge,
+                           min(peak_gflops, ai_flop_per_byte * peak_gbs))
+
+
+@dataclass(frozen=True)
+class HistogramBin:
+    lo: float
+    hi: float
+    count: int
+
+
+def make_histogram(result: TuningResult, bins: int) -> List[HistogramBin]:
+    """reference tuner.cpp:263-290: equal-width gflops bins over [min, max];
+    the maximum lands in the last bin, a flat population in the first."""
+    if bins == 0:
+        raise ValueError("need at least one histogram bin")
+    if not result.records:
+        raise ValueError("no records to bin")
+    g = [r.gflops for r in result.records]
+    lo, hi = min(g), max(g)
+    width = (hi - lo) / bins
+    edges = [(lo + width * i, hi if i + 1 == bins else lo + width * (i + 1)) for i in range(bins)]
+    counts = [0] * bins
+    for x in g:
+        counts[min(int((x - lo) / width), bins - 1) if width > 0.0 else 0] += 1
+    return [HistogramBin(a, b, n) for (a, b), n in zip(edges, counts)]
+
+
+# ------------------------------------------------ tuning-result documents --
+TUNING_SCHEMA = "dedisp-tuning-result/1"
+
+
+def tuning_result_to_dict(result: TuningResult, threads: int = 1) -> dict:
+    """The reference's tuning-result document (report_io.cpp:58-102: same
+    keys, same order, schema "dedisp-tuning-result/1") so its `analyze`
+    subcommand and tuning_result_from_json read GPU results unchanged.  The
+    GPU knobs of each record ride in an extra "b200" object, which the
+    reference parser ignores; `threads` is the host-thread field (1: the
+    device sweep is sequential)."""
+    s = result.setup
+    recs = []
+    for r in result.records:
+        k = r.config
+        recs.append({"items_time": k.items_time, "items_dm": k.items_dm,
+                     "work_time": k.work_time, "work_dm": k.work_dm,
+                     "runs_s": list(r.runs), "mean_time_s": r.mean_time, "gflops": r.gflops,
+                     "timer_warning": r.timer_warning,
+                     "b200": {"dm_tile_depth": r.dm_tile_depth, "staging": r.staging,
+                              "family": r.family, "flags": r.flags}})
+    st = result.stats
+    return {
+        "schema": TUNING_SCHEMA,
+        "setup": {"name": s.name, "samples_per_second": s.samples_per_second,
+                  "channels": s.channels, "f_min_mhz": s.f_min,
+                  "channel_width_mhz": s.channel_width, "dm_first": s.dm_first,
+                  "dm_step": s.dm_step},
+        "num_dms": result.num_dms,
+        "zero_dm": result.zero_dm,
+        "limits": {"max_block_items": result.limits.max_block_items,
+                   "max_accumulators": result.limits.max_accumulators},
+        "repeats": result.repeats,
+        "seed": result.seed,
+        "environment": {"threads": threads, "rng": result.rng_id,
+                        "clock_resolution_s": result.clock_resolution_s},
+        "records": recs,
+        "best_index": result.best_index,
+        "stats": {"mean_gflops": st.mean_gflops, "stddev_gflops": st.stddev_gflops,
+                  "snr_optimum": st.snr_optimum, "chebyshev_bound": st.chebyshev_bound,
+                  "degenerate": st.degenerate},
+        "realtime": {"threshold_gflops": result.realtime_threshold_gflops,
+                     "pass": result.realtime_pass},
+    }
+
+
+def tuning_result_to_json(result: TuningResult, threads: int = 1) -> str:
+    return json.dumps(tuning_result_to_dict(result, threads), indent=2) + "\n"
+
+
+class FormatError(ValueError):
+    """reference errors.hpp format_error"""
+
+
+def tuning_result_from_json(text: str) -> TuningResult:
+    """reference report_io.cpp:104-156: every key it requires is required
+    here; a document without "b200" record objects (the CPU reference's own)
+    loads with default GPU knobs."""
+    try:
+        doc = json.loads(text)
+        if doc["schema"] != TUNING_SCHEMA:
+            raise FormatError(f"unrecognized schema '{doc['schema']}'")
+        s = doc["setup"]
+        setup = ObservationSetup(s["name"], int(s["samples_per_second"]), int(s["channels"]),
+                                 float(s["f_min_mhz"]), float(s["channel_width_mhz"]),
+                                 float(s["dm_first"]), float(s["dm_step"]))
+        recs = []
+        for n in doc["records"]:
+            x = n.get("b200", {})
+            recs.append(TuningRecord(KernelConfig(int(n["items_time"]), int(n["items_dm"]),
+                                                  int(n["work_time"]), int(n["work_dm"])),
+                                     [float(v) for v in n["runs_s"]], float(n["mean_time_s"]),
+                                     float(n["gflops"]), bool(n["timer_warning"]),
+                                     int(x.get("dm_tile_depth", 1)), x.get("staging", "auto"),
+                                     x.get("family", ""), int(x.get("flags", 0))))
+        best = int(doc["best_index"])
+        if not recs or best >= len(recs):
+            raise FormatError("best_index does not point into records")
+        st = doc["stats"]
+        stats = TuningStats(float(st["mean_gflops"]), float(st["stddev_gflops"]),
+                            st["snr_optimum"], st["chebyshev_bound"], bool(st["degenerate"]))
+        env = doc["environment"]
+        res = TuningResult(setup, int(doc["num_dms"]), bool(doc["zero_dm"]),
+                           KernelLimits(int(doc["limits"]["max_block_items"]),
+                                        int(doc["limits"]["max_accumulators"])),
+                           int(doc["repeats"]), int(doc["seed"]), recs, best, stats,
+                           float(doc["realtime"]["threshold_gflops"]),
+                           bool(doc["realtime"]["pass"]), env["rng"],
+                           float(env["clock_resolution_s"]))
+        int(env["threads"])
+        return res
+    except FormatError:
+        raise
+    except (ValueError, KeyError, TypeError, AttributeError) as e:
+        raise FormatError(f"bad tuning-result document: {e!r}") from None
+
+
+def tuning_result_to_csv(result: TuningResult) -> str:
+    """reference report_io.cpp:166-176"""
+    rows = ["items_time,items_dm,work_time,work_dm,mean_time_s,gflops"]
+    for r in result.records:
+        k = r.config
+        rows.append(f"{k.items_time},{k.items_dm},{k.work_time},{k.work_dm},"
+                    f"{r.mean_time:.17g},{r.gflops:.17g}")
+    return "\n".join(rows) + "\n"

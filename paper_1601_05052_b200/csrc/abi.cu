@@ -374,7 +374,7 @@ dd_status dd_validate_config(const dd_config* k, uint32_t num_dms, uint32_t s,
     return fail(DD_ERR_INVALID_ARGUMENT, "work_time * work_dm exceeds the accumulator limit of " +
                                              std::to_string(L.max_accumulators));
   if (k->staging > DD_STAGING_TMEM) return fail(DD_ERR_INVALID_ARGUMENT, "unknown staging mode");
-  if (k->flags & ~(DD_CONFIG_GPU_TILING | DD_CONFIG_CPS_MASK))
+  if (k->flags & ~(DD_CONFIG_GPU_TILING | DD_CONFIG_HIGH_OCCUPANCY | DD_CONFIG_CPS_MASK))
     return fail(DD_ERR_INVALID_ARGUMENT, "unknown config flags");
   if (((k->flags & DD_CONFIG_CPS_MASK) >> DD_CONFIG_CPS_SHIFT) > 8)
     return fail(DD_ERR_INVALID_ARGUMENT, "channels per stage must be 1..8");
@@ -391,10 +391,12 @@ dd_status dd_count_loads(const uint32_t* sh, uint32_t channels, uint32_t num_dms
     return fail(DD_ERR_INVALID_ARGUMENT, "kernel config parameters must all be positive");
   const uint64_t tt = static_cast<uint64_t>(k->items_time) * k->work_time;
   const uint64_t td = static_cast<uint64_t>(k->items_dm) * k->work_dm;
-  if (tt > s || s % tt != 0 || td > num_dms || num_dms % td != 0)
+  // DD_CONFIG_GPU_TILING: the predicated last time tile stages like a full one
+  const bool gpu_tiling = (k->flags & DD_CONFIG_GPU_TILING) != 0;
+  if (tt > s || (s % tt != 0 && !gpu_tiling) || td > num_dms || num_dms % td != 0)
     return fail(DD_ERR_INVALID_ARGUMENT, "kernel config does not tile this instance");
   uint64_t st = 0, id = 0;
-  const uint64_t tiles_time = s / tt;
+  const uint64_t tiles_time = (s + tt - 1) / tt;
   for (uint64_t dm0 = 0; dm0 < num_dms; dm0 += td)
     for (uint32_t ch = 0; ch < channels; ++ch) {
       uint32_t lo = sh[dm0 * channels + ch], hi = lo;
@@ -613,7 +615,7 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
     if (e == cudaSuccess) e = cudaMemsetAsync(c->d_scratch, 0, 16, c->stream);
     if (e == cudaSuccess)
       e = launch_plan(d_shifts, p->d_rec, p->d_ls, c->d_scratch, d_sum, channels, a.tiles_dm, a.tile_dm,
-                      k->work_dm, a.rec_bytes, c->stream);
+                      k->work_dm, a.rec_bytes, k->staging == DD_STAGING_TMEM, c->stream);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(scratch, c->d_scratch, 16, cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
@@ -639,7 +641,12 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
       fn = find_regwin_kernel(k->work_dm, k->work_time, p->group_span, &p->regwin_span);
       slack = p->regwin_span + 4;
     } else if (family == DD_STAGING_TMEM) {
-      fn = find_tmem_kernel(k->work_dm, k->work_time, p->group_span, &p->regwin_span);
+      // three-CTA build when the CTA is <= 4 consumer warps and one exists
+      const bool small = (k->flags & DD_CONFIG_HIGH_OCCUPANCY) && ((block + 31) & ~31ull) + 32 <= 160;
+      fn = small ? find_tmem_kernel(k->work_dm, k->work_time, p->group_span, &p->regwin_span, true)
+                 : nullptr;
+      if (fn == nullptr)
+        fn = find_tmem_kernel(k->work_dm, k->work_time, p->group_span, &p->regwin_span);
       slack = p->regwin_span + 8;
     } else {
       fn = find_smem_kernel(k->work_dm, k->work_time);
@@ -738,6 +745,14 @@ dd_status dd_plan_get_info(const dd_plan* p, dd_plan_info* info) {
   info->stages = p->args.nstage;
   info->kernel_launches = 1;
   info->staged_bytes = p->staged_bytes;
+  if (p->smem_fn != nullptr) {
+    cudaFuncAttributes fa{};
+    int ctas = 0;
+    if (cudaFuncGetAttributes(&fa, p->smem_fn) == cudaSuccess) info->registers = fa.numRegs;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, p->smem_fn, static_cast<int>(p->threads),
+                                                      p->smem) == cudaSuccess)
+      info->ctas_per_sm = static_cast<uint32_t>(ctas);
+  }
   if (p->reference_order) {
     const uint64_t n = static_cast<uint64_t>(p->args.num_dms) * p->args.s;
     info->grid_x = static_cast<uint32_t>((n + 255) / 256);

@@ -122,7 +122,7 @@ struct PlanRec {
 // below it) -- the register/TMEM-window kernels' fast-path test, precomputed.
 __host__ __device__ inline uint32_t plan_rec_bytes(uint32_t tile_dm, uint32_t group = 1) {
   const uint32_t groups = (tile_dm + group - 1) / group;
-  return ((16u + 4u * tile_dm + 4u * groups) + 15u) & ~15u;
+  return ((16u + 4u * tile_dm + 8u * groups) + 15u) & ~15u;
 }
 
 struct TiledArgs {

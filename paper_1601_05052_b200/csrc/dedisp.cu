@@ -528,12 +528,41 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(
+                   taddr),
+               "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]),
+               "f"(v[7])
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
+      "f"(v[15])
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
                  "=f"(r[6]), "=f"(r[7])
                : "r"(taddr)
                : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]),
+        "=f"(r[7]), "=f"(r[8]), "=f"(r[9]), "=f"(r[10]), "=f"(r[11]), "=f"(r[12]), "=f"(r[13]),
+        "=f"(r[14]), "=f"(r[15])
+      : "r"(taddr)
+      : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* r) {
@@ -552,10 +581,17 @@ __device__ __forceinline__ void tmem_wait_ld() {
 
 template <int K, int W, int SPAN, int COLS>
 struct TmemBody {
-  static_assert(W % 4 == 0 && (W / 4) % 2 == 1, "W/4 odd: conflict-free 16-byte loads");
+  static_assert(W % 4 == 0, "16-byte window loads (W/4 odd is conflict-free, even is 2-way)");
   static_assert(COLS == 32 || COLS == 64, "32 or 64 TMEM columns per warp window");
   static_assert(W + SPAN + 3 <= COLS, "window must fit the warp's TMEM columns");
   static_assert(K % 2 == 0, "DMs are read back in pairs");
+  // W = 12: read each DM with one x16 load; the 4 extra columns may run past
+  // the warp's window (tmem_cols_for allocates the slack) and are ignored.
+  static constexpr bool kOver = false;
+  // window columns beyond the first 32: 0, 8, 16 or 32
+  static constexpr int kNeed = W + SPAN + 3 - 32;
+  static constexpr int kTail = kNeed <= 0 ? 0 : kNeed <= 8 ? 8 : kNeed <= 16 ? 16 : 32;
+  static_assert(kTail == 0 || COLS == 64, "windows past 32 columns need 64 per warp");
   const TiledArgs& a;
   uint32_t col, dml, taddr;
   float acc[K][W];
@@ -574,25 +610,43 @@ struct TmemBody {
 #pragma unroll
       for (int j = 0; j < W; ++j) acc[k][j] = 0.0f;
   }
-  // Per-channel state fetched from shared memory one channel ahead.
+  // Per-channel state fetched from shared memory.
   struct Pre {
-    uint32_t off[K];
-    uint32_t spread, al, nv;
-    const float* base;
+    uint32_t off[K];  // window columns of the warp's DMs (k_plan window format)
+    uint32_t nv;      // 16-byte window vectors to stage; 0 = slow path
+    const float* base;  // this lane's 16-byte aligned window start
     float win[32];  // first 32 window columns (fast path)
   };
 
   // Offsets + (fast) the first half of the window: only the 16-byte vectors
   // the warp's DMs actually span this channel (nv, warp-uniform) are read.
+  // k_plan's window format (table.cu) precomputes the columns relative to
+  // the aligned window start, the alignment and the start itself.
   __device__ __forceinline__ void fetch(Pre& n, const uint32_t* r, const float* w) const {
+    if constexpr (K % 4 == 0) {
+      const uint4* o = reinterpret_cast<const uint4*>(r + 4 + dml);
 #pragma unroll
-    for (int k = 0; k < K; ++k) n.off[k] = r[4 + dml + k];
-    n.spread = r[4 + a.tile_dm + dml / K];  // precomputed by k_plan
-    n.base = w + col;
-    const float* p = n.base + n.off[0];
-    n.al = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p) >> 2) & 3u;
-    n.nv = n.spread <= static_cast<uint32_t>(SPAN) ? (n.al + n.spread + W + 3) >> 2 : 0u;
-    const float* pa = p - n.al;
+      for (int k = 0; k < K; k += 4) {
+        const uint4 v = o[k / 4];
+        n.off[k] = v.x;
+        n.off[k + 1] = v.y;
+        n.off[k + 2] = v.z;
+        n.off[k + 3] = v.w;
+      }
+    } else {
+      const uint2* o = reinterpret_cast<const uint2*>(r + 4 + dml);
+#pragma unroll
+      for (int k = 0; k < K; k += 2) {
+        const uint2 v = o[k / 2];
+        n.off[k] = v.x;
+        n.off[k + 1] = v.y;
+      }
+    }
+    const uint2 g = *reinterpret_cast<const uint2*>(r + 4 + a.tile_dm + 2 * (dml / K));
+    const uint32_t spread = g.x & 0x3fffffffu;
+    n.nv = spread <= static_cast<uint32_t>(SPAN) ? ((g.x >> 30) + spread + W + 3) >> 2 : 0u;
+    n.base = w + col + static_cast<int32_t>(g.y);
+    const float* pa = n.base;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
       lds128_if(static_cast<uint32_t>(i) < n.nv, pa + 4 * i, n.win[4 * i], n.win[4 * i + 1],
@@ -600,35 +654,46 @@ struct TmemBody {
   }
 
   // Window -> this lane's TMEM row; afterwards n.win may be refilled.
-  __device__ __forceinline__ void commit(const Pre& n) const {
+  __device__ __forceinline__ void commit(Pre& n) const {
     if (n.nv == 0) return;
     tmem_st32(taddr, n.win);
-    if constexpr (COLS == 64) {
+    if constexpr (kTail > 0) {
+      // columns 32.. of the widest window (alignment + SPAN + W): an x8,
+      // x16 or x32 store sized at compile time keeps the extra live
+      // registers to what the variant can need
       if (n.nv > 8) {
-        const float* pa = n.base + n.off[0] - n.al + 32;
-        float hi[32];
+        // reuse the head's registers once the x32 store has read them
+        const float* pa = n.base + 32;
+        float* hi = n.win;
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < kTail / 4; ++i)
           lds128_if(static_cast<uint32_t>(i) < n.nv - 8, pa + 4 * i, hi[4 * i], hi[4 * i + 1],
                     hi[4 * i + 2], hi[4 * i + 3]);
-        tmem_st32(taddr + 32, hi);
+        if constexpr (kTail == 8) tmem_st8(taddr + 32, hi);
+        else if constexpr (kTail == 16) tmem_st16(taddr + 32, hi);
+        else tmem_st32(taddr + 32, hi);
       }
     }
     tmem_wait_st();
   }
 
-  __device__ __forceinline__ void accumulate(const uint32_t (&off)[K], uint32_t al, bool fast,
+  __device__ __forceinline__ void accumulate(const uint32_t (&off)[K], bool fast,
                                              const float* base) {
     if (fast) {
 #pragma unroll
       for (int k = 0; k < K; k += 2) {
-        float v[2][W];
+        float v[2][kOver ? W + 4 : W];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const uint32_t c = taddr + al + off[k + h] - off[0];
+          const uint32_t c = taddr + off[k + h];
+          if constexpr (kOver) {
+            // one x16 load per DM (4 unused columns) instead of x8 + x4
+            tmem_ld16(c, v[h]);
+          } else {
 #pragma unroll
-          for (int j = 0; j + 8 <= W; j += 8) tmem_ld8(c + j, &v[h][j]);
-          if constexpr (W % 8 == 4) tmem_ld4(c + (W - 4), &v[h][W - 4]);
+            for (int j = 0; j + 8 <= W; j += 8) tmem_ld8(c + j, &v[h][j]);
+            if constexpr (W % 8 == 4) tmem_ld4(c + (W - W % 8), &v[h][W - W % 8]);
+          }
         }
         tmem_wait_ld();
 #pragma unroll
@@ -660,7 +725,7 @@ struct TmemBody {
     Pre n;
     fetch(n, r, w);
     commit(n);
-    accumulate(n.off, n.al, n.nv != 0, n.base);
+    accumulate(n.off, n.nv != 0, n.base);
   }
   __device__ __forceinline__ void load(uint32_t dm0, uint32_t t0) {
 #pragma unroll
@@ -683,8 +748,9 @@ struct TmemBody {
 
 // TMEM columns per CTA: `cols` per consumer warp beyond the 4 lane
 // quarters, rounded to the allocator's power of two (>= 32).
-__device__ __forceinline__ uint32_t tmem_cols_for(uint32_t consumer_warps, uint32_t per_warp) {
-  const uint32_t need = ((consumer_warps + 3) / 4) * per_warp;
+__device__ __forceinline__ uint32_t tmem_cols_for(uint32_t consumer_warps, uint32_t per_warp,
+                                                  uint32_t over) {
+  const uint32_t need = ((consumer_warps + 3) / 4) * per_warp + over;
   uint32_t cols = 32;
   while (cols < need) cols <<= 1;
   return cols;
@@ -695,7 +761,7 @@ __device__ __forceinline__ void tmemwin_run(const TiledArgs& a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint32_t tmem_base;
   const uint32_t consumers = blockDim.x / 32 - 1;
-  const uint32_t cols = tmem_cols_for(consumers, COLS);
+  const uint32_t cols = tmem_cols_for(consumers, COLS, TmemBody<K, W, SPAN, COLS>::kOver ? 4 : 0);
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_addr(&tmem_base)),
@@ -717,6 +783,13 @@ __device__ __forceinline__ void tmemwin_run(const TiledArgs& a) {
 
 template <int K, int W, int SPAN, int COLS>
 __global__ void __launch_bounds__(288) k_tmemwin(const TiledArgs a) {
+  tmemwin_run<K, W, SPAN, COLS>(a);
+}
+
+// Occupancy build for CTAs of <= 4 consumer warps + the producer: three CTAs
+// per SM (<= 136 registers) instead of two.
+template <int K, int W, int SPAN, int COLS>
+__global__ void __launch_bounds__(160, 3) k_tmemwin_occ(const TiledArgs a) {
   tmemwin_run<K, W, SPAN, COLS>(a);
 }
 
@@ -786,20 +859,27 @@ KernelFn find_regwin_kernel(uint32_t k, uint32_t w, uint32_t group_span, uint32_
 struct TmemVariant {
   int k, w, span;
   KernelFn fn;
+  KernelFn fn_occ;  // <= 160 threads, 3 CTAs/SM; nullptr when not built
 };
 
-#define DDB_T(K, W, S, C) {K, W, S, k_tmemwin<K, W, S, C>}
+#define DDB_T(K, W, S, C) {K, W, S, k_tmemwin<K, W, S, C>, nullptr}
+#define DDB_TO(K, W, S, C) {K, W, S, k_tmemwin<K, W, S, C>, k_tmemwin_occ<K, W, S, C>}
 static const TmemVariant kTmemVariants[] = {
-    DDB_T(2, 12, 8, 32),  DDB_T(4, 12, 12, 32), DDB_T(4, 12, 16, 32), DDB_T(8, 12, 16, 32),
-    DDB_T(8, 12, 32, 64), DDB_T(2, 20, 8, 32),  DDB_T(4, 20, 8, 32),  DDB_T(4, 20, 24, 64),
+    DDB_T(2, 12, 8, 32),  DDB_TO(4, 12, 12, 32), DDB_T(4, 12, 16, 32), DDB_T(8, 12, 16, 32),
+    DDB_T(8, 12, 24, 64), DDB_T(8, 12, 32, 64), DDB_T(2, 20, 8, 32),   DDB_T(4, 20, 8, 32),  DDB_T(4, 20, 24, 64),
+    DDB_T(8, 8, 32, 64),  DDB_T(16, 4, 48, 64),  DDB_TO(8, 4, 24, 32), DDB_TO(4, 4, 8, 32),
+    DDB_TO(4, 8, 12, 32),
 };
 #undef DDB_T
+#undef DDB_TO
 
-KernelFn find_tmem_kernel(uint32_t k, uint32_t w, uint32_t group_span, uint32_t* span_out) {
+KernelFn find_tmem_kernel(uint32_t k, uint32_t w, uint32_t group_span, uint32_t* span_out,
+                          bool occ) {
   const TmemVariant* cover = nullptr;
   const TmemVariant* widest = nullptr;
   for (const TmemVariant& v : kTmemVariants) {
     if (static_cast<uint32_t>(v.k) != k || static_cast<uint32_t>(v.w) != w) continue;
+    if (occ && v.fn_occ == nullptr) continue;
     if (widest == nullptr || v.span > widest->span) widest = &v;
     if (static_cast<uint32_t>(v.span) >= group_span && (cover == nullptr || v.span < cover->span))
       cover = &v;
@@ -807,13 +887,19 @@ KernelFn find_tmem_kernel(uint32_t k, uint32_t w, uint32_t group_span, uint32_t*
   const TmemVariant* pick = cover ? cover : widest;
   if (pick == nullptr) return nullptr;
   if (span_out) *span_out = static_cast<uint32_t>(pick->span);
-  return pick->fn;
+  return occ ? pick->fn_occ : pick->fn;
 }
 
 bool tmem_shape_ok(uint32_t k, uint32_t w, uint32_t items_time, uint64_t block) {
   if (items_time % 32 != 0 || block > 256) return false;
   for (const TmemVariant& v : kTmemVariants)
     if (static_cast<uint32_t>(v.k) == k && static_cast<uint32_t>(v.w) == w) return true;
+  return false;
+}
+
+bool tmem_has_occupancy_build(uint32_t k, uint32_t w) {
+  for (const TmemVariant& v : kTmemVariants)
+    if (static_cast<uint32_t>(v.k) == k && static_cast<uint32_t>(v.w) == w && v.fn_occ) return true;
   return false;
 }
 
@@ -848,8 +934,16 @@ cudaError_t launch_smem(KernelFn fn, const TiledArgs& a, uint32_t blocks, uint32
 }
 
 cudaError_t prepare_smem(KernelFn fn, uint32_t smem) {
-  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(smem));
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  // The staged kernels never read through L1 (TMA fills shared memory,
+  // outputs are streaming stores): ask for the whole unified array as
+  // shared memory so the register budget, not the carveout, sets the
+  // resident CTAs per SM.
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+  return e;
 }
 
 }  // namespace ddb

@@ -49,7 +49,8 @@ cudaError_t launch_delay_table(uint32_t* d_shifts, uint32_t* d_max, uint32_t num
                                double dm_first, double dm_step, double rate, cudaStream_t st);
 cudaError_t launch_plan(const uint32_t* d_shifts, uint8_t* d_rec, uint2* d_ls, uint32_t* d_max_span,
                         unsigned long long* d_span_sum, uint32_t channels, uint32_t tiles_dm,
-                        uint32_t tile_dm, uint32_t group, uint32_t rec_bytes, cudaStream_t st);
+                        uint32_t tile_dm, uint32_t group, uint32_t rec_bytes, uint32_t window_format,
+                        cudaStream_t st);
 cudaError_t launch_max_u32(const uint32_t* d_v, uint64_t n, uint32_t* d_out, cudaStream_t st);
 
 using KernelFn = void (*)(const TiledArgs);
@@ -60,8 +61,10 @@ KernelFn find_smem_kernel(uint32_t k, uint32_t w, uint32_t* max_threads = nullpt
 // (or the widest one); *span_out = its SPAN.  nullptr when not instantiated.
 KernelFn find_regwin_kernel(uint32_t k, uint32_t w, uint32_t group_span, uint32_t* span_out);
 bool regwin_shape_ok(uint32_t k, uint32_t w, uint32_t items_time, uint64_t block);
-KernelFn find_tmem_kernel(uint32_t k, uint32_t w, uint32_t group_span, uint32_t* span_out);
+KernelFn find_tmem_kernel(uint32_t k, uint32_t w, uint32_t group_span, uint32_t* span_out,
+                          bool occ = false);
 bool tmem_shape_ok(uint32_t k, uint32_t w, uint32_t items_time, uint64_t block);
+bool tmem_has_occupancy_build(uint32_t k, uint32_t w);
 // True when the staged family can run cfg (block size within the variant's cap).
 inline bool smem_variant_ok(uint32_t k, uint32_t w, uint64_t block) {
   uint32_t cap = 0;

@@ -49,7 +49,7 @@ __global__ void k_delay_table(uint32_t* __restrict__ shifts, uint32_t* __restric
 __global__ void k_plan(const uint32_t* __restrict__ shifts, uint8_t* __restrict__ rec,
                        uint2* __restrict__ ls, uint32_t* __restrict__ max_span, unsigned long long* __restrict__ span_sum,
                        uint32_t channels, uint32_t tiles_dm, uint32_t tile_dm, uint32_t group,
-                       uint32_t rec_bytes) {
+                       uint32_t rec_bytes, uint32_t window_format) {
   const uint64_t n = static_cast<uint64_t>(tiles_dm) * channels;
   const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   uint32_t span = 0, gspan = 0;
@@ -76,13 +76,25 @@ __global__ void k_plan(const uint32_t* __restrict__ shifts, uint8_t* __restrict_
       bool below = false;
       for (uint32_t l = g0; l < g0 + group && l < tile_dm; ++l) {
         const uint32_t v = col[static_cast<uint64_t>(l) * channels];
-        r[4 + l] = v - lo;
+        // window format (TMEM windows): offsets from the group's 16-byte
+        // aligned window start, so the first is the alignment itself
+        r[4 + l] = window_format ? v - (first & ~3u) : v - lo;
         glo = min(glo, v);
         ghi = max(ghi, v);
         below = below || v < first;
       }
       gspan = max(gspan, ghi - glo);
-      r[4 + tile_dm + g0 / group] = below ? 0xffffffffu : ghi - first;
+      uint32_t* gr = r + 4 + tile_dm + 2 * (g0 / group);
+      if (window_format) {
+        // {spread | alignment << 30, aligned window start relative to the
+        //  consumer's row pointer (which sits at lo & 3)}
+        const uint32_t spread = below ? 0x3fffffffu : min(ghi - first, 0x3ffffffeu);
+        gr[0] = spread | ((first & 3u) << 30);
+        gr[1] = (first & ~3u) - lo;  // two's complement when negative
+      } else {
+        gr[0] = below ? 0xffffffffu : ghi - first;
+        gr[1] = 0;
+      }
     }
   }
   const uint32_t sum = __reduce_add_sync(0xffffffffu, span);
@@ -128,13 +140,15 @@ cudaError_t launch_delay_table(uint32_t* d_shifts, uint32_t* d_max, uint32_t num
 
 cudaError_t launch_plan(const uint32_t* d_shifts, uint8_t* d_rec, uint2* d_ls, uint32_t* d_max_span,
                         unsigned long long* d_span_sum, uint32_t channels, uint32_t tiles_dm,
-                        uint32_t tile_dm, uint32_t group, uint32_t rec_bytes, cudaStream_t st) {
+                        uint32_t tile_dm, uint32_t group, uint32_t rec_bytes, uint32_t window_format,
+                        cudaStream_t st) {
   const uint64_t n = static_cast<uint64_t>(tiles_dm) * channels;
   const uint32_t threads = 128;
   const uint64_t blocks = (n + threads - 1) / threads;
   k_plan<<<static_cast<uint32_t>(blocks), threads, 0, st>>>(d_shifts, d_rec, d_ls, d_max_span,
                                                             d_span_sum, channels, tiles_dm, tile_dm,
-                                                            group ? group : 1, rec_bytes);
+                                                            group ? group : 1, rec_bytes,
+                                                            window_format);
   return cudaGetLastError();
 }
 

@@ -213,6 +213,10 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
               c.staging = DD_STAGING_TMEM;
               c.flags = DD_CONFIG_GPU_TILING | (cps << DD_CONFIG_CPS_SHIFT);
               v.push_back(c);
+              if (block <= 128 && tmem_has_occupancy_build(wd, wt)) {
+                c.flags |= DD_CONFIG_HIGH_OCCUPANCY;
+                v.push_back(c);
+              }
             }
           }
           if (regwin_shape_ok(wd, wt, it, block)) {

@@ -33,7 +33,8 @@ def main():
             extra = f[6:]
             p = ctx.plan(sh.data_ptr(), c, d, s, t, t, cfg, int(f[4]), f[5],
                          gpu_tiling="g" in extra,
-                         stage_channels=next((int(x[3:]) for x in extra if x.startswith("cps")), 0))
+                         stage_channels=next((int(x[3:]) for x in extra if x.startswith("cps")), 0),
+                         high_occupancy="occ" in extra)
         except ValueError as e:
             print(f"{spec:28s} invalid: {e}")
             continue
@@ -41,7 +42,8 @@ def main():
         ms = sorted(runs)[len(runs) // 2] * 1e3
         i = p.info()
         print(f"{spec:28s} {i['family']:7s} {ms:8.3f} ms  {flop / ms / 1e6:9.1f} GFLOP/s  "
-              f"smem={i['smem_bytes']} stages={i['stages']}x{i['channels_per_stage']}", flush=True)
+              f"smem={i['smem_bytes']} stages={i['stages']}x{i['channels_per_stage']} "
+              f"regs={i['registers']} ctas/sm={i['ctas_per_sm']}", flush=True)
 
 
 if __name__ == "__main__":

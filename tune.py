@@ -7,9 +7,13 @@ dedisp_tune.cpp:464-535, on the device).
 For every instance it benchmarks every configuration of the chosen space on
 the GPU (1 warm-up + `repeats` CUDA-event-timed runs, tuner.cpp:136-170),
 selects the optimum (tuner.cpp:172-179), computes the population statistics
-(tuner.cpp:181-206), and writes tuning/<setup>_<d>.json.  With several
-instances it also reports best_fixed_config and the tuned-vs-fixed speedups
-(tuner.cpp:218-261; BASELINE config 5) in tuning/<setup>_summary.json.
+(tuner.cpp:181-206), and writes tuning/<setup>_<d>[_zerodm].json in the
+reference's "dedisp-tuning-result/1" layout (report_io.cpp:58-102; GPU knobs
+in per-record "b200" objects, roofline and sweep time in a top-level "b200"
+object), so tools/analyze.py -- the reference's `analyze` -- reads them.
+With several instances it also reports best_fixed_config and the
+tuned-vs-fixed speedups (tuner.cpp:218-261; BASELINE config 5) in
+tuning/<setup>_summary.json.
 """
 from __future__ import annotations
 
@@ -25,31 +29,14 @@ sys.path.insert(0, ROOT)
 from paper_1601_05052_b200 import api  # noqa: E402
 
 
-def record_json(r: api.TuningRecord) -> dict:
-    c = r.config
-    return {"items_time": c.items_time, "items_dm": c.items_dm, "work_time": c.work_time,
-            "work_dm": c.work_dm, "dm_tile_depth": r.dm_tile_depth, "staging": r.staging,
-            "flags": r.flags, "stage_channels": r.stage_channels,
-            "family": r.family, "mean_time": r.mean_time, "gflops": r.gflops,
-            "timer_warning": r.timer_warning}
-
-
 def result_json(res: api.TuningResult, hbm_gbs: float, seconds: float) -> dict:
     d, s, c = res.num_dms, res.setup.samples_per_second, res.setup.channels
-    best = record_json(res.best())
-    best["hbm_roofline_gflops"] = api.roofline_gflops(d, s, c, hbm_gbs)
-    best["roofline_frac"] = best["gflops"] / best["hbm_roofline_gflops"]
-    return {
-        "schema": "dedisp-tuning-result/1+b200",
-        "setup": res.setup.__dict__, "num_dms": d, "zero_dm": res.zero_dm,
-        "limits": res.limits.__dict__, "repeats": res.repeats, "seed": res.seed,
-        "rng_id": res.rng_id, "clock": "cuda events", "clock_resolution_s": res.clock_resolution_s,
-        "best_index": res.best_index, "best": best,
-        "stats": res.stats.__dict__,
-        "realtime_threshold_gflops": res.realtime_threshold_gflops,
-        "realtime_pass": res.realtime_pass, "sweep_seconds": seconds,
-        "records": [record_json(r) for r in res.records],
-    }
+    doc = api.tuning_result_to_dict(res)
+    best = res.best()
+    roof = api.roofline_gflops(d, s, c, hbm_gbs)
+    doc["b200"] = {"clock": "cuda events", "sweep_seconds": seconds, "hbm_gbs": hbm_gbs,
+                   "hbm_roofline_gflops": roof, "best_roofline_frac": best.gflops / roof}
+    return doc
 
 
 def main():
@@ -78,16 +65,15 @@ def main():
         dt = time.time() - t0
         results.append(res)
         j = result_json(res, hbm, dt)
-        name = f"{setup.name.lower()}_{d}{'_zero' if a.zero_dm else ''}.json"
+        name = f"{setup.name.lower()}_{d}{'_zerodm' if a.zero_dm else ''}.json"
         with open(os.path.join(a.out, name), "w") as f:
             json.dump(j, f, indent=1)
-        b = j["best"]
+        b, k = res.best(), res.best().config
         print(f"{setup.name} d={d}: {len(res.records)} configs in {dt:.1f}s; best "
-              f"({b['items_time']},{b['items_dm']},{b['work_time']},{b['work_dm']}) "
-              f"depth={b['dm_tile_depth']} {b['staging']} cps={b['stage_channels']}: "
-              f"{b['gflops']:.1f} GFLOP/s "
-              f"({b['mean_time'] * 1e3:.3f} ms, {b['roofline_frac']:.2f}x HBM roofline); "
-              f"snr={res.stats.snr_optimum}", flush=True)
+              f"({k.items_time},{k.items_dm},{k.work_time},{k.work_dm}) "
+              f"depth={b.dm_tile_depth} {b.staging} flags={b.flags:#x}: {b.gflops:.1f} GFLOP/s "
+              f"({b.mean_time * 1e3:.3f} ms, {j['b200']['best_roofline_frac']:.2f}x HBM "
+              f"roofline); snr={res.stats.snr_optimum}", flush=True)
     if len(results) > 1:
         rep = api.best_fixed_config(results)
         k, depth, staging, flags = rep.config
@@ -98,7 +84,7 @@ def main():
                 "fixed_gflops": rep.fixed_gflops, "tuned_gflops": [r.best().gflops for r in results],
                 "speedup_over_fixed": rep.speedup_over_fixed}
         with open(os.path.join(a.out, f"{setup.name.lower()}_summary"
-                               f"{'_zero' if a.zero_dm else ''}.json"), "w") as f:
+                               f"{'_zerodm' if a.zero_dm else ''}.json"), "w") as f:
             json.dump(summ, f, indent=1)
         print("best fixed:", summ["best_fixed"], "speedups:",
               [round(x, 3) for x in rep.speedup_over_fixed])
