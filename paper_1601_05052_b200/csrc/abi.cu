@@ -461,7 +461,7 @@ bool smem_geometry(const dd_context* c, uint32_t tile_time, uint32_t tile_dm, ui
     for (uint32_t ns : ns_opts) {
       for (uint32_t cp : cps_opts) {
         if (cp > channels && cp != 1) continue;
-        const uint64_t bytes = 128 + static_cast<uint64_t>(ns) * cp * slot;
+        const uint64_t bytes = ddb::kPipeHeader + static_cast<uint64_t>(ns) * cp * slot;
         if (bytes <= budget && bytes <= limit) {
           *win_cap = static_cast<uint32_t>(wc);
           *rec_bytes = static_cast<uint32_t>(rb);
@@ -615,7 +615,8 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
     if (e == cudaSuccess) e = cudaMemsetAsync(c->d_scratch, 0, 16, c->stream);
     if (e == cudaSuccess)
       e = launch_plan(d_shifts, p->d_rec, p->d_ls, c->d_scratch, d_sum, channels, a.tiles_dm, a.tile_dm,
-                      k->work_dm, a.rec_bytes, k->staging == DD_STAGING_TMEM, c->stream);
+                      k->work_dm, a.rec_bytes,
+                      k->staging == DD_STAGING_TMEM ? k->work_time : 0u, c->stream);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(scratch, c->d_scratch, 16, cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
@@ -641,10 +642,10 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
       fn = find_regwin_kernel(k->work_dm, k->work_time, p->group_span, &p->regwin_span);
       slack = p->regwin_span + 4;
     } else if (family == DD_STAGING_TMEM) {
-      // three-CTA build when the CTA is <= 4 consumer warps and one exists
-      const bool small = (k->flags & DD_CONFIG_HIGH_OCCUPANCY) && ((block + 31) & ~31ull) + 32 <= 160;
-      fn = small ? find_tmem_kernel(k->work_dm, k->work_time, p->group_span, &p->regwin_span, true)
-                 : nullptr;
+      // three-CTA builds when the CTA is <= 4 consumer warps and one exists
+      const bool small = ((block + 31) & ~31ull) + 32 <= 160;
+      if (small && (k->flags & DD_CONFIG_HIGH_OCCUPANCY))
+        fn = find_tmem_kernel(k->work_dm, k->work_time, p->group_span, &p->regwin_span, true);
       if (fn == nullptr)
         fn = find_tmem_kernel(k->work_dm, k->work_time, p->group_span, &p->regwin_span);
       slack = p->regwin_span + 8;

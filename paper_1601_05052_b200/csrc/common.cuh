@@ -48,6 +48,19 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 
 // 16-byte shared load under a predicate; the destination keeps its old
 // contents when the predicate is off (no zero-fill instructions).
+// As lds128_if, but the destination's previous value is declared dead: with
+// the predicate off the registers hold unspecified values.  For staging
+// buffers whose unloaded tail is never read, this lets the register
+// allocator reuse them between uses (the "+f" form keeps them live).
+__device__ __forceinline__ void lds128_maybe(bool pred, const float* addr, float& x, float& y,
+                                             float& z, float& w) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "@q ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n\t}"
+      : "=f"(x), "=f"(y), "=f"(z), "=f"(w)
+      : "r"(smem_addr(addr)), "r"(static_cast<int>(pred)));
+}
+
 __device__ __forceinline__ void lds128_if(bool pred, const float* addr, float& x, float& y,
                                           float& z, float& w) {
   asm volatile(
@@ -124,6 +137,10 @@ __host__ __device__ inline uint32_t plan_rec_bytes(uint32_t tile_dm, uint32_t gr
   const uint32_t groups = (tile_dm + group - 1) / group;
   return ((16u + 4u * tile_dm + 8u * groups) + 15u) & ~15u;
 }
+
+// Staged-kernel shared-memory header: full[8] and empty[8] mbarriers;
+// records and windows follow.
+constexpr uint32_t kPipeHeader = 128;
 
 struct TiledArgs {
   const float* in;

@@ -111,7 +111,7 @@ __device__ __forceinline__ Pipe pipe_setup(const TiledArgs& a, uint8_t* smem) {
   Pipe p;
   p.full = reinterpret_cast<uint64_t*>(smem);
   p.empty = reinterpret_cast<uint64_t*>(smem + 64);
-  p.recs = smem + 128;
+  p.recs = smem + kPipeHeader;
   p.wins = reinterpret_cast<float*>(p.recs + a.nstage * a.cps * a.rec_bytes);
   const uint32_t groups_dm = (a.tiles_dm + a.depth - 1) / a.depth;
   p.t0 = (blockIdx.x / groups_dm) * a.tile_time;
@@ -241,7 +241,10 @@ __device__ __forceinline__ void staged_loop_with(const TiledArgs& a, uint8_t* sm
     if (active) {
       for (uint32_t cc = 0; cc < ncs; ++cc) {
         const uint32_t* r = reinterpret_cast<const uint32_t*>(rbase + cc * a.rec_bytes);
-        body.channel(r, wbase + cc * a.win_cap + ((p.t0 + r[0]) & 3u));
+        if constexpr (Body::kRowBase)
+          body.channel(r, wbase + cc * a.win_cap);
+        else
+          body.channel(r, wbase + cc * a.win_cap + ((p.t0 + r[0]) & 3u));
       }
     }
     __syncwarp();
@@ -265,6 +268,7 @@ __device__ __forceinline__ void staged_loop(const TiledArgs& a, uint8_t* smem) {
 // ---------------------------------------------------------------------
 template <int K, int W>
 struct SmemBody {
+  static constexpr bool kRowBase = false;  // channel() gets the row at lo's sample
   const TiledArgs& a;
   uint32_t it, id;
   float acc[K][W];
@@ -450,6 +454,7 @@ struct RegWin {
 // warps, and warp-level parallelism hides the shared-memory latency better.
 template <int K, int W, int SPAN>
 struct RegWinBody {
+  static constexpr bool kRowBase = false;
   const TiledArgs& a;
   uint32_t col;  // first sample of this lane relative to t0
   uint32_t dml;  // first DM of this warp relative to dm0
@@ -581,6 +586,7 @@ __device__ __forceinline__ void tmem_wait_ld() {
 
 template <int K, int W, int SPAN, int COLS>
 struct TmemBody {
+  static constexpr bool kRowBase = true;  // channel() gets the 16-byte aligned row start
   static_assert(W % 4 == 0, "16-byte window loads (W/4 odd is conflict-free, even is 2-way)");
   static_assert(COLS == 32 || COLS == 64, "32 or 64 TMEM columns per warp window");
   static_assert(W + SPAN + 3 <= COLS, "window must fit the warp's TMEM columns");
@@ -643,13 +649,13 @@ struct TmemBody {
       }
     }
     const uint2 g = *reinterpret_cast<const uint2*>(r + 4 + a.tile_dm + 2 * (dml / K));
-    const uint32_t spread = g.x & 0x3fffffffu;
-    n.nv = spread <= static_cast<uint32_t>(SPAN) ? ((g.x >> 30) + spread + W + 3) >> 2 : 0u;
-    n.base = w + col + static_cast<int32_t>(g.y);
+    // fast iff the window fits the columns this variant stages
+    n.nv = g.x <= static_cast<uint32_t>((32 + kTail) / 4) ? g.x : 0u;
+    n.base = w + col + g.y;  // w: the channel's 16-byte aligned row (kRowBase)
     const float* pa = n.base;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
-      lds128_if(static_cast<uint32_t>(i) < n.nv, pa + 4 * i, n.win[4 * i], n.win[4 * i + 1],
+      lds128_maybe(static_cast<uint32_t>(i) < n.nv, pa + 4 * i, n.win[4 * i], n.win[4 * i + 1],
                 n.win[4 * i + 2], n.win[4 * i + 3]);
   }
 
@@ -667,7 +673,7 @@ struct TmemBody {
         float* hi = n.win;
 #pragma unroll
         for (int i = 0; i < kTail / 4; ++i)
-          lds128_if(static_cast<uint32_t>(i) < n.nv - 8, pa + 4 * i, hi[4 * i], hi[4 * i + 1],
+          lds128_maybe(static_cast<uint32_t>(i) < n.nv - 8, pa + 4 * i, hi[4 * i], hi[4 * i + 1],
                     hi[4 * i + 2], hi[4 * i + 3]);
         if constexpr (kTail == 8) tmem_st8(taddr + 32, hi);
         else if constexpr (kTail == 16) tmem_st16(taddr + 32, hi);
@@ -690,6 +696,7 @@ struct TmemBody {
             // one x16 load per DM (4 unused columns) instead of x8 + x4
             tmem_ld16(c, v[h]);
           } else {
+#pragma unroll
 #pragma unroll
             for (int j = 0; j + 8 <= W; j += 8) tmem_ld8(c + j, &v[h][j]);
             if constexpr (W % 8 == 4) tmem_ld4(c + (W - W % 8), &v[h][W - W % 8]);
@@ -866,7 +873,8 @@ struct TmemVariant {
 #define DDB_TO(K, W, S, C) {K, W, S, k_tmemwin<K, W, S, C>, k_tmemwin_occ<K, W, S, C>}
 static const TmemVariant kTmemVariants[] = {
     DDB_T(2, 12, 8, 32),  DDB_TO(4, 12, 12, 32), DDB_T(4, 12, 16, 32), DDB_T(8, 12, 16, 32),
-    DDB_T(8, 12, 24, 64), DDB_T(8, 12, 32, 64), DDB_T(2, 20, 8, 32),   DDB_T(4, 20, 8, 32),  DDB_T(4, 20, 24, 64),
+    DDB_T(8, 12, 24, 64), DDB_T(8, 12, 32, 64), DDB_T(2, 20, 8, 32),  DDB_T(4, 20, 8, 32),
+    DDB_T(4, 20, 24, 64),
     DDB_T(8, 8, 32, 64),  DDB_T(16, 4, 48, 64),  DDB_TO(8, 4, 24, 32), DDB_TO(4, 4, 8, 32),
     DDB_TO(4, 8, 12, 32),
 };

@@ -86,11 +86,11 @@ __global__ void k_plan(const uint32_t* __restrict__ shifts, uint8_t* __restrict_
       gspan = max(gspan, ghi - glo);
       uint32_t* gr = r + 4 + tile_dm + 2 * (g0 / group);
       if (window_format) {
-        // {spread | alignment << 30, aligned window start relative to the
-        //  consumer's row pointer (which sits at lo & 3)}
-        const uint32_t spread = below ? 0x3fffffffu : min(ghi - first, 0x3ffffffeu);
-        gr[0] = spread | ((first & 3u) << 30);
-        gr[1] = (first & ~3u) - lo;  // two's complement when negative
+        // {16-byte vectors the window spans (alignment + spread + W, W =
+        //  window_format), or ~0 for a group below its first DM (slow path);
+        //  aligned window start relative to the 16-byte aligned row start}
+        gr[0] = below ? 0xffffffffu : ((first & 3u) + (ghi - first) + window_format + 3u) >> 2;
+        gr[1] = (first & ~3u) - (lo & ~3u);
       } else {
         gr[0] = below ? 0xffffffffu : ghi - first;
         gr[1] = 0;

@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
+from paper_1601_05052_b200 import _native as N
 from paper_1601_05052_b200 import api
 
 pytestmark = pytest.mark.gpu
@@ -250,15 +251,16 @@ def test_non_monotone_and_fault_injected_tables(dev, golden):
     ("tmem", K(32, 4, 12, 4), 8), ("tmem", K(32, 8, 12, 4), 4), ("tmem", K(64, 2, 12, 2), 8),
     ("tmem", K(32, 4, 20, 2), 8), ("tmem", K(32, 4, 12, 8), 4), ("tmem", K(32, 8, 20, 4), 8),
     ("tmem", K(32, 4, 4, 8), 8), ("tmem", K(32, 2, 4, 16), 8), ("tmem", K(32, 4, 8, 8), 4),
-    ("tmem", K(32, 4, 4, 8), 8, True), ("tmem", K(32, 4, 12, 4), 8, True),
-    ("tmem", K(32, 4, 4, 4), 4, True), ("tmem", K(32, 4, 8, 4), 8, True)])
+    ("tmem", K(32, 4, 4, 8), 8, "occ"), ("tmem", K(32, 4, 12, 4), 8, "occ"),
+    ("tmem", K(32, 4, 4, 4), 4, "occ"), ("tmem", K(32, 4, 8, 4), 8, "occ"),
+    ("tmem", K(32, 2, 12, 8), 3), ("tmem", K(32, 1, 12, 8), 1), ("tmem", K(32, 4, 20, 4), 2)])
 def test_gpu_tiling_predicated_tail(dev, golden, spec):
     """GPU-native tiles whose tile_time does not divide s (vector register
     windows, odd smem tiles, TMEM windows incl. the three-CTA builds): the
     predicated last tile must not change a bit."""
     import torch
     staging, cfg, cps = spec[:3]
-    occ = len(spec) > 3
+    mode = spec[3] if len(spec) > 3 else ""
     g = golden["baseline"][0]
     setup, table, fb = _golden_instance(g)
     d, s, c, t = g["num_dms"], setup.samples_per_second, setup.channels, g["num_samples"]
@@ -268,10 +270,11 @@ def test_gpu_tiling_predicated_tail(dev, golden, spec):
     out = torch.full((d, s), float("nan"), device="cuda")
     torch.cuda.synchronize()
     p = dev.plan(sh.data_ptr(), c, d, s, t, t, cfg, 1, staging, gpu_tiling=True,
-                 stage_channels=cps, high_occupancy=occ)
-    assert p.info()["family"] == staging
-    if occ:
-        assert 0 < p.info()["registers"] <= 128
+                 stage_channels=cps, high_occupancy=mode == "occ")
+    info = p.info()
+    assert info["family"] == staging
+    if mode == "occ":
+        assert 0 < info["registers"] <= 128
     p.execute(x.data_ptr(), out.data_ptr())
     dev.synchronize()
     assert O.fnv1a(out.cpu().numpy()) == g["out_fnv"]

@@ -3,7 +3,7 @@
     python tools/time_configs.py Apertif 4096 "32,4,25,4,1,regwin" "16,16,10,4,1,smem" ...
 
 Extra fields: "g" requests GPU tiling (tile_time need not divide s),
-"cpsN" pins N channels per pipeline stage.
+"cpsN" pins N channels per pipeline stage, "occ" the TMEM three-CTA build.
 """
 import os
 import sys
