@@ -91,11 +91,15 @@ typedef struct dd_config {
  * <= 4 consumer warps per CTA) when one exists for the shape; otherwise the
  * flag is ignored.  A tuning knob: occupancy against register pressure. */
 #define DD_CONFIG_HIGH_OCCUPANCY 0x2u
-/* Staged families: channels per pipeline stage in bits 8..11 (1..8; 0 lets
+/* Staged families: channels per pipeline stage in bits 8..11 (1..15; 0 lets
  * the plan choose).  A tuning knob: larger stages amortise the per-stage
  * synchronisation, smaller ones leave shared memory for more CTAs per SM. */
 #define DD_CONFIG_CPS_SHIFT 8u
 #define DD_CONFIG_CPS_MASK (0xfu << DD_CONFIG_CPS_SHIFT)
+/* Staged families: pipeline depth (stages in flight) in bits 12..15 (2..8;
+ * 0 lets the plan choose).  A tuning knob like the stage width. */
+#define DD_CONFIG_NSTAGE_SHIFT 12u
+#define DD_CONFIG_NSTAGE_MASK (0xfu << DD_CONFIG_NSTAGE_SHIFT)
 
 /* KernelLimits (kernels.hpp:31-34); {0,0} means the reference defaults
  * {1024, 256}. */

@@ -20,6 +20,8 @@ DD_CONFIG_GPU_TILING = 0x1
 DD_CONFIG_HIGH_OCCUPANCY = 0x2
 DD_CONFIG_CPS_SHIFT = 8
 DD_CONFIG_CPS_MASK = 0xF << DD_CONFIG_CPS_SHIFT
+DD_CONFIG_NSTAGE_SHIFT = 12
+DD_CONFIG_NSTAGE_MASK = 0xF << DD_CONFIG_NSTAGE_SHIFT
 
 
 class CapacityError(RuntimeError):

@@ -374,10 +374,12 @@ dd_status dd_validate_config(const dd_config* k, uint32_t num_dms, uint32_t s,
     return fail(DD_ERR_INVALID_ARGUMENT, "work_time * work_dm exceeds the accumulator limit of " +
                                              std::to_string(L.max_accumulators));
   if (k->staging > DD_STAGING_TMEM) return fail(DD_ERR_INVALID_ARGUMENT, "unknown staging mode");
-  if (k->flags & ~(DD_CONFIG_GPU_TILING | DD_CONFIG_HIGH_OCCUPANCY | DD_CONFIG_CPS_MASK))
+  if (k->flags &
+      ~(DD_CONFIG_GPU_TILING | DD_CONFIG_HIGH_OCCUPANCY | DD_CONFIG_CPS_MASK | DD_CONFIG_NSTAGE_MASK))
     return fail(DD_ERR_INVALID_ARGUMENT, "unknown config flags");
-  if (((k->flags & DD_CONFIG_CPS_MASK) >> DD_CONFIG_CPS_SHIFT) > 8)
-    return fail(DD_ERR_INVALID_ARGUMENT, "channels per stage must be 1..8");
+
+  const uint32_t ns = (k->flags & DD_CONFIG_NSTAGE_MASK) >> DD_CONFIG_NSTAGE_SHIFT;
+  if (ns == 1 || ns > 8) return fail(DD_ERR_INVALID_ARGUMENT, "pipeline stages must be 2..8");
   return DD_OK;
 }
 
@@ -435,7 +437,7 @@ constexpr uint32_t kSmemBudget = 112 * 1024;  // aim for 2 CTAs per SM
 // `slack` floats per window: the register-window kernel reads up to SPAN
 // samples past a window (never added), which must stay inside the slot.
 bool smem_geometry(const dd_context* c, uint32_t tile_time, uint32_t tile_dm, uint32_t group,
-                   uint32_t channels, uint32_t max_span, uint32_t slack, uint32_t want_cps,
+                   uint32_t channels, uint32_t max_span, uint32_t slack, uint32_t flags,
                    uint32_t* win_cap,
                    uint32_t* rec_bytes, uint32_t* cps, uint32_t* nstage, uint32_t* smem) {
   const uint64_t wc =
@@ -448,14 +450,17 @@ bool smem_geometry(const dd_context* c, uint32_t tile_time, uint32_t tile_dm, ui
   // DEDISP_B200_STAGE_CPS / _NSTAGE pin the shape (tuning experiments).
   uint32_t cps_opts[] = {8, 4, 2, 1};
   uint32_t ns_opts[] = {3, 2};
-  if (want_cps >= 1 && want_cps <= 8) cps_opts[0] = want_cps;
+  const uint32_t want_cps = (flags & DD_CONFIG_CPS_MASK) >> DD_CONFIG_CPS_SHIFT;
+  const uint32_t want_ns = (flags & DD_CONFIG_NSTAGE_MASK) >> DD_CONFIG_NSTAGE_SHIFT;
+  if (want_cps >= 1) cps_opts[0] = want_cps;
+  if (want_ns >= 2 && want_ns <= 8) ns_opts[0] = want_ns;
   if (const char* e = std::getenv("DEDISP_B200_STAGE_CPS")) {
     const uint32_t v = static_cast<uint32_t>(std::atoi(e));
-    if (v >= 1 && v <= 8) cps_opts[0] = v;
+    if (v >= 1 && v <= 15) cps_opts[0] = v;
   }
   if (const char* e = std::getenv("DEDISP_B200_STAGE_NSTAGE")) {
     const uint32_t v = static_cast<uint32_t>(std::atoi(e));
-    if (v >= 2 && v <= 4) ns_opts[0] = v;
+    if (v >= 2 && v <= 8) ns_opts[0] = v;
   }
   for (uint64_t budget : {static_cast<uint64_t>(kSmemBudget), limit}) {
     for (uint32_t ns : ns_opts) {
@@ -500,7 +505,7 @@ dd_status dd_config_family(dd_context* c, const dd_config* k, uint32_t channels,
   if (smem_ok) {
     uint32_t a, b, cc, d, e;
     smem_ok = smem_geometry(c, tile_time, tile_dm, k->work_dm, channels, max_span, 0,
-                            (k->flags & DD_CONFIG_CPS_MASK) >> DD_CONFIG_CPS_SHIFT, &a, &b,
+                            k->flags, &a, &b,
                             &cc, &d, &e);
   }
   switch (k->staging) {
@@ -661,7 +666,7 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
       fn = nullptr;
     if (fn != nullptr &&
         smem_geometry(c, a.tile_time, a.tile_dm, k->work_dm, channels, p->max_span, slack,
-                      (k->flags & DD_CONFIG_CPS_MASK) >> DD_CONFIG_CPS_SHIFT, &win_cap,
+                      k->flags, &win_cap,
                       &rec_bytes, &cps, &nstage, &smem)) {
       a.win_cap = win_cap;
       a.cps = cps;

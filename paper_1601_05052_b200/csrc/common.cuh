@@ -29,6 +29,12 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
+// Raise the phase's expected transaction bytes without arriving.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+
 // Plain arrival (release, CTA scope): a consumer warp hands a slot back.
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
@@ -138,6 +144,8 @@ __host__ __device__ inline uint32_t plan_rec_bytes(uint32_t tile_dm, uint32_t gr
   return ((16u + 4u * tile_dm + 8u * groups) + 15u) & ~15u;
 }
 
+// Channels per pipeline stage: 1..kMaxCps (DD_CONFIG_CPS_* holds 1..15).
+constexpr uint32_t kMaxCps = 16;
 // Staged-kernel shared-memory header: full[8] and empty[8] mbarriers;
 // records and windows follow.
 constexpr uint32_t kPipeHeader = 128;

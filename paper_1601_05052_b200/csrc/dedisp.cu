@@ -125,7 +125,7 @@ __device__ __forceinline__ Pipe pipe_setup(const TiledArgs& a, uint8_t* smem) {
 // (lo, span) of the up-to-8 channels of chunk g, fetched one chunk ahead
 // by the producer so the global-memory latency overlaps its slot wait.
 struct ChunkSpans {
-  uint2 v[8];
+  uint2 v[kMaxCps];
 };
 
 __device__ __forceinline__ ChunkSpans pipe_spans(const TiledArgs& a, const Pipe& p, uint32_t g) {
@@ -135,7 +135,10 @@ __device__ __forceinline__ ChunkSpans pipe_spans(const TiledArgs& a, const Pipe&
   const uint32_t ncs = min(a.cps, a.ch_end - ch0);
   const uint2* src = a.ls + static_cast<uint64_t>(b) * a.channels + ch0;
 #pragma unroll
-  for (uint32_t cc = 0; cc < 8; ++cc) c.v[cc] = cc < ncs ? __ldg(src + cc) : make_uint2(0, 0);
+  for (uint32_t cc = 0; cc < kMaxCps; ++cc) {
+    if (cc >= ncs) break;  // a branch, not kMaxCps predicated loads
+    c.v[cc] = __ldg(src + cc);
+  }
   return c;
 }
 
@@ -148,29 +151,27 @@ __device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, ui
   const uint32_t ncs = min(a.cps, a.ch_end - ch0);
   const uint32_t slot = g % a.nstage;
   const uint8_t* rsrc = a.rec + (static_cast<uint64_t>(b) * a.channels + ch0) * a.rec_bytes;
-  uint32_t start[8], bytes[8];
-  uint32_t total = ncs * a.rec_bytes;
+  uint64_t* bar = &p.full[slot];
+  // Each copy first raises the phase's expected bytes; the closing arrival
+  // (the phase's only one) cannot complete it before every copy is counted.
+  mbar_expect_tx(bar, ncs * a.rec_bytes);
+  bulk_g2s(p.recs + slot * a.cps * a.rec_bytes, rsrc, ncs * a.rec_bytes, bar);
+  const float* src = a.in + blockIdx.y * a.in_beam_stride + static_cast<uint64_t>(ch0) * a.in_pitch;
+  float* dst = p.wins + static_cast<uint64_t>(slot * a.cps) * a.win_cap;
 #pragma unroll
-  for (uint32_t cc = 0; cc < 8; ++cc) {
+  for (uint32_t cc = 0; cc < kMaxCps; ++cc) {
+    if (cc >= ncs) break;
     const uint32_t lo = cs.v[cc].x, span = cs.v[cc].y;
-    start[cc] = (p.t0 + lo) & ~3u;
+    const uint32_t start = (p.t0 + lo) & ~3u;
     // a predicated last time tile must not read past the (pitched) row
     const uint32_t end = min((p.t0 + lo + span + a.tile_time + 3u) & ~3u,
                              static_cast<uint32_t>(a.in_pitch));
-    bytes[cc] = cc < ncs ? (end - start[cc]) * 4u : 0u;
-    total += bytes[cc];
+    const uint32_t bytes = (end - start) * 4u;
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(dst + static_cast<uint64_t>(cc) * a.win_cap, src + static_cast<uint64_t>(cc) * a.in_pitch + start,
+             bytes, bar);
   }
-  mbar_arrive_expect_tx(&p.full[slot], total);
-  bulk_g2s(p.recs + slot * a.cps * a.rec_bytes, rsrc, ncs * a.rec_bytes, &p.full[slot]);
-#pragma unroll
-  for (uint32_t cc = 0; cc < 8; ++cc) {
-    if (cc < ncs)
-      bulk_g2s(p.wins + static_cast<uint64_t>(slot * a.cps + cc) * a.win_cap,
-               a.in + blockIdx.y * a.in_beam_stride + static_cast<uint64_t>(ch0 + cc) * a.in_pitch +
-                   start[cc],
-               bytes[cc],
-               &p.full[slot]);
-  }
+  mbar_arrive(bar);
 }
 
 // The producer lane: issue every chunk as soon as its slot is handed back.
@@ -683,9 +684,41 @@ struct TmemBody {
     tmem_wait_st();
   }
 
+  static constexpr bool kPipe = false;
+  __device__ __forceinline__ void load_pair(const uint32_t (&off)[K], int k, float (&v)[2][W]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t c = taddr + off[k + h];
+#pragma unroll
+      for (int j = 0; j + 8 <= W; j += 8) tmem_ld8(c + j, &v[h][j]);
+      if constexpr (W % 8 == 4) tmem_ld4(c + (W - W % 8), &v[h][W - W % 8]);
+    }
+  }
+  __device__ __forceinline__ void add_pair(int k, float (&v)[2][W]) {
+    tmem_wait_ld();
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int j = 0; j < W; j += 2) {
+        const float2 s2 = fadd2(make_float2(acc[k + h][j], acc[k + h][j + 1]),
+                                make_float2(v[h][j], v[h][j + 1]));
+        acc[k + h][j] = s2.x;
+        acc[k + h][j + 1] = s2.y;
+      }
+  }
   __device__ __forceinline__ void accumulate(const uint32_t (&off)[K], bool fast,
                                              const float* base) {
-    if (fast) {
+    if (fast && kPipe) {
+      // software-pipelined: the next DM pair's loads are issued before the
+      // current pair's adds
+      float v[2][2][W];
+      load_pair(off, 0, v[0]);
+#pragma unroll
+      for (int k = 0; k < K; k += 2) {
+        if (k + 2 < K) load_pair(off, k + 2, v[((k / 2) + 1) & 1]);
+        add_pair(k, v[(k / 2) & 1]);
+      }
+    } else if (fast) {
 #pragma unroll
       for (int k = 0; k < K; k += 2) {
         float v[2][kOver ? W + 4 : W];

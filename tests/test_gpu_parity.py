@@ -253,7 +253,9 @@ def test_non_monotone_and_fault_injected_tables(dev, golden):
     ("tmem", K(32, 4, 4, 8), 8), ("tmem", K(32, 2, 4, 16), 8), ("tmem", K(32, 4, 8, 8), 4),
     ("tmem", K(32, 4, 4, 8), 8, "occ"), ("tmem", K(32, 4, 12, 4), 8, "occ"),
     ("tmem", K(32, 4, 4, 4), 4, "occ"), ("tmem", K(32, 4, 8, 4), 8, "occ"),
-    ("tmem", K(32, 2, 12, 8), 3), ("tmem", K(32, 1, 12, 8), 1), ("tmem", K(32, 4, 20, 4), 2)])
+    ("tmem", K(32, 2, 12, 8), 3), ("tmem", K(32, 1, 12, 8), 1), ("tmem", K(32, 4, 20, 4), 2),
+    ("tmem", K(32, 4, 12, 8), 15), ("tmem", K(32, 4, 12, 8), 11), ("smem", K(32, 4, 4, 4), 13),
+    ("regwin", K(32, 4, 12, 4), 15)])
 def test_gpu_tiling_predicated_tail(dev, golden, spec):
     """GPU-native tiles whose tile_time does not divide s (vector register
     windows, odd smem tiles, TMEM windows incl. the three-CTA builds): the
@@ -272,7 +274,7 @@ def test_gpu_tiling_predicated_tail(dev, golden, spec):
     p = dev.plan(sh.data_ptr(), c, d, s, t, t, cfg, 1, staging, gpu_tiling=True,
                  stage_channels=cps, high_occupancy=mode == "occ")
     info = p.info()
-    assert info["family"] == staging
+    assert info["family"] == staging and info["channels_per_stage"] == cps
     if mode == "occ":
         assert 0 < info["registers"] <= 128
     p.execute(x.data_ptr(), out.data_ptr())

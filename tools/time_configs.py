@@ -3,7 +3,8 @@
     python tools/time_configs.py Apertif 4096 "32,4,25,4,1,regwin" "16,16,10,4,1,smem" ...
 
 Extra fields: "g" requests GPU tiling (tile_time need not divide s),
-"cpsN" pins N channels per pipeline stage, "occ" the TMEM three-CTA build.
+"cpsN" pins N channels per pipeline stage, "occ" the TMEM three-CTA build,
+"nsN" N pipeline stages.
 """
 import os
 import sys
@@ -11,6 +12,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
+from paper_1601_05052_b200 import _native as N  # noqa: E402
 from paper_1601_05052_b200 import api  # noqa: E402
 
 
@@ -34,7 +36,9 @@ def main():
             p = ctx.plan(sh.data_ptr(), c, d, s, t, t, cfg, int(f[4]), f[5],
                          gpu_tiling="g" in extra,
                          stage_channels=next((int(x[3:]) for x in extra if x.startswith("cps")), 0),
-                         high_occupancy="occ" in extra)
+                         high_occupancy="occ" in extra,
+                         flags=next((int(x[2:]) for x in extra if x.startswith("ns")), 0)
+                         << N.DD_CONFIG_NSTAGE_SHIFT)
         except ValueError as e:
             print(f"{spec:28s} invalid: {e}")
             continue
