@@ -173,7 +173,7 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
     if (!(k.items_time % 32 == 0 || k.items_time == 8 || k.items_time == 16)) continue;
     const uint32_t tiles_dm = num_dms / (k.items_dm * k.work_dm);
     if (regwin_shape_ok(k.work_dm, k.work_time, k.items_time, block)) {
-      for (uint32_t cps : {4u, 8u}) {
+      for (uint32_t cps : {8u, 15u}) {
         dd_config c = k;
         c.dm_tile_depth = 1;
         c.staging = DD_STAGING_REGWIN;
@@ -184,7 +184,7 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
     if (block < 64 || !smem_variant_ok(k.work_dm, k.work_time, block)) continue;
     for (uint32_t depth : {1u, 2u}) {
       if (depth > 1 && tiles_dm < depth * 2) continue;
-      for (uint32_t cps : {4u, 8u}) {
+      for (uint32_t cps : {8u, 15u}) {
         dd_config c = k;
         c.dm_tile_depth = depth;
         c.staging = DD_STAGING_SMEM;
@@ -209,11 +209,13 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
           if (s % (it * wt) == 0) continue;  // already in the reference space
           dd_config c{it, idm, wt, wd, 1, DD_STAGING_REGWIN, DD_CONFIG_GPU_TILING};
           if (tmem_shape_ok(wd, wt, it, block)) {
-            for (uint32_t cps : {4u, 8u}) {
+            // wide stages amortise the per-stage synchronisation; the
+            // three-CTA builds need the narrower stages' shared memory
+            for (uint32_t cps : {8u, 15u}) {
               c.staging = DD_STAGING_TMEM;
               c.flags = DD_CONFIG_GPU_TILING | (cps << DD_CONFIG_CPS_SHIFT);
               v.push_back(c);
-              if (block <= 128 && tmem_has_occupancy_build(wd, wt)) {
+              if (cps == 8 && block <= 128 && tmem_has_occupancy_build(wd, wt)) {
                 c.flags |= DD_CONFIG_HIGH_OCCUPANCY;
                 v.push_back(c);
               }
@@ -221,7 +223,7 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
           }
           if (regwin_shape_ok(wd, wt, it, block)) {
             c.staging = DD_STAGING_REGWIN;
-            c.flags = DD_CONFIG_GPU_TILING | (4u << DD_CONFIG_CPS_SHIFT);
+            c.flags = DD_CONFIG_GPU_TILING | (8u << DD_CONFIG_CPS_SHIFT);
             v.push_back(c);
           }
         }
