@@ -560,17 +560,6 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* r) {
                : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
-      "%12, %13, %14, %15}, [%16];"
-      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]),
-        "=f"(r[7]), "=f"(r[8]), "=f"(r[9]), "=f"(r[10]), "=f"(r[11]), "=f"(r[12]), "=f"(r[13]),
-        "=f"(r[14]), "=f"(r[15])
-      : "r"(taddr)
-      : "memory");
-}
-
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
                : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3])
@@ -585,16 +574,14 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int K, int W, int SPAN, int COLS>
+template <int K, int W, int SPAN, int COLS, bool FULL_HEAD = true>
 struct TmemBody {
   static constexpr bool kRowBase = true;  // channel() gets the 16-byte aligned row start
   static_assert(W % 4 == 0, "16-byte window loads (W/4 odd is conflict-free, even is 2-way)");
   static_assert(COLS == 32 || COLS == 64, "32 or 64 TMEM columns per warp window");
   static_assert(W + SPAN + 3 <= COLS, "window must fit the warp's TMEM columns");
   static_assert(K % 2 == 0, "DMs are read back in pairs");
-  // W = 12: read each DM with one x16 load; the 4 extra columns may run past
-  // the warp's window (tmem_cols_for allocates the slack) and are ignored.
-  static constexpr bool kOver = false;
+  static constexpr bool kFullHead = FULL_HEAD;
   // window columns beyond the first 32: 0, 8, 16 or 32
   static constexpr int kNeed = W + SPAN + 3 - 32;
   static constexpr int kTail = kNeed <= 0 ? 0 : kNeed <= 8 ? 8 : kNeed <= 16 ? 16 : 32;
@@ -654,10 +641,25 @@ struct TmemBody {
     n.nv = g.x <= static_cast<uint32_t>((32 + kTail) / 4) ? g.x : 0u;
     n.base = w + col + g.y;  // w: the channel's 16-byte aligned row (kRowBase)
     const float* pa = n.base;
+    if constexpr (kFullHead) {
+      // all 8 head vectors, unpredicated: columns past the window are never
+      // read back, the slot's slack keeps the reads inside shared memory,
+      // and unconditional definitions let the allocator retire the staging
+      // registers between channels (predicated ones keep them live)
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      lds128_maybe(static_cast<uint32_t>(i) < n.nv, pa + 4 * i, n.win[4 * i], n.win[4 * i + 1],
-                n.win[4 * i + 2], n.win[4 * i + 3]);
+      for (int i = 0; i < 8; ++i) {
+        const float4 v = *reinterpret_cast<const float4*>(pa + 4 * i);
+        n.win[4 * i] = v.x;
+        n.win[4 * i + 1] = v.y;
+        n.win[4 * i + 2] = v.z;
+        n.win[4 * i + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        lds128_maybe(static_cast<uint32_t>(i) < n.nv, pa + 4 * i, n.win[4 * i],
+                     n.win[4 * i + 1], n.win[4 * i + 2], n.win[4 * i + 3]);
+    }
   }
 
   // Window -> this lane's TMEM row; afterwards n.win may be refilled.
@@ -684,56 +686,20 @@ struct TmemBody {
     tmem_wait_st();
   }
 
-  static constexpr bool kPipe = false;
-  __device__ __forceinline__ void load_pair(const uint32_t (&off)[K], int k, float (&v)[2][W]) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const uint32_t c = taddr + off[k + h];
-#pragma unroll
-      for (int j = 0; j + 8 <= W; j += 8) tmem_ld8(c + j, &v[h][j]);
-      if constexpr (W % 8 == 4) tmem_ld4(c + (W - W % 8), &v[h][W - W % 8]);
-    }
-  }
-  __device__ __forceinline__ void add_pair(int k, float (&v)[2][W]) {
-    tmem_wait_ld();
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int j = 0; j < W; j += 2) {
-        const float2 s2 = fadd2(make_float2(acc[k + h][j], acc[k + h][j + 1]),
-                                make_float2(v[h][j], v[h][j + 1]));
-        acc[k + h][j] = s2.x;
-        acc[k + h][j + 1] = s2.y;
-      }
-  }
   __device__ __forceinline__ void accumulate(const uint32_t (&off)[K], bool fast,
                                              const float* base) {
-    if (fast && kPipe) {
-      // software-pipelined: the next DM pair's loads are issued before the
-      // current pair's adds
-      float v[2][2][W];
-      load_pair(off, 0, v[0]);
+    if (fast) {
+      // (ptxas schedules the loads itself: with the staging registers free
+      // between channels it keeps 3-4 of them in flight)
 #pragma unroll
       for (int k = 0; k < K; k += 2) {
-        if (k + 2 < K) load_pair(off, k + 2, v[((k / 2) + 1) & 1]);
-        add_pair(k, v[(k / 2) & 1]);
-      }
-    } else if (fast) {
-#pragma unroll
-      for (int k = 0; k < K; k += 2) {
-        float v[2][kOver ? W + 4 : W];
+        float v[2][W];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const uint32_t c = taddr + off[k + h];
-          if constexpr (kOver) {
-            // one x16 load per DM (4 unused columns) instead of x8 + x4
-            tmem_ld16(c, v[h]);
-          } else {
 #pragma unroll
-#pragma unroll
-            for (int j = 0; j + 8 <= W; j += 8) tmem_ld8(c + j, &v[h][j]);
-            if constexpr (W % 8 == 4) tmem_ld4(c + (W - W % 8), &v[h][W - W % 8]);
-          }
+          for (int j = 0; j + 8 <= W; j += 8) tmem_ld8(c + j, &v[h][j]);
+          if constexpr (W % 8 == 4) tmem_ld4(c + (W - W % 8), &v[h][W - W % 8]);
         }
         tmem_wait_ld();
 #pragma unroll
@@ -788,20 +754,20 @@ struct TmemBody {
 
 // TMEM columns per CTA: `cols` per consumer warp beyond the 4 lane
 // quarters, rounded to the allocator's power of two (>= 32).
-__device__ __forceinline__ uint32_t tmem_cols_for(uint32_t consumer_warps, uint32_t per_warp,
-                                                  uint32_t over) {
-  const uint32_t need = ((consumer_warps + 3) / 4) * per_warp + over;
+__device__ __forceinline__ uint32_t tmem_cols_for(uint32_t consumer_warps, uint32_t per_warp) {
+  const uint32_t need = ((consumer_warps + 3) / 4) * per_warp;
   uint32_t cols = 32;
   while (cols < need) cols <<= 1;
   return cols;
 }
 
-template <int K, int W, int SPAN, int COLS>
+template <int K, int W, int SPAN, int COLS, bool FULL_HEAD = true>
 __device__ __forceinline__ void tmemwin_run(const TiledArgs& a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint32_t tmem_base;
   const uint32_t consumers = blockDim.x / 32 - 1;
-  const uint32_t cols = tmem_cols_for(consumers, COLS, TmemBody<K, W, SPAN, COLS>::kOver ? 4 : 0);
+  using Body = TmemBody<K, W, SPAN, COLS, FULL_HEAD>;
+  const uint32_t cols = tmem_cols_for(consumers, COLS);
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_addr(&tmem_base)),
@@ -812,7 +778,7 @@ __device__ __forceinline__ void tmemwin_run(const TiledArgs& a) {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  staged_loop_with<TmemBody<K, W, SPAN, COLS>>(a, smem, tmem_base);
+  staged_loop_with<Body>(a, smem, tmem_base);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -830,7 +796,7 @@ __global__ void __launch_bounds__(288) k_tmemwin(const TiledArgs a) {
 // per SM (<= 136 registers) instead of two.
 template <int K, int W, int SPAN, int COLS>
 __global__ void __launch_bounds__(160, 3) k_tmemwin_occ(const TiledArgs a) {
-  tmemwin_run<K, W, SPAN, COLS>(a);
+  tmemwin_run<K, W, SPAN, COLS, false>(a);  // predicated head: fewer live registers
 }
 
 // ------------------------------------------------------------ dispatch --
@@ -905,7 +871,7 @@ struct TmemVariant {
 #define DDB_T(K, W, S, C) {K, W, S, k_tmemwin<K, W, S, C>, nullptr}
 #define DDB_TO(K, W, S, C) {K, W, S, k_tmemwin<K, W, S, C>, k_tmemwin_occ<K, W, S, C>}
 static const TmemVariant kTmemVariants[] = {
-    DDB_T(2, 12, 8, 32),  DDB_TO(4, 12, 12, 32), DDB_T(4, 12, 16, 32), DDB_T(8, 12, 16, 32),
+    DDB_T(2, 12, 8, 32),  DDB_TO(4, 12, 12, 32), DDB_T(4, 12, 16, 32),
     DDB_T(8, 12, 24, 64), DDB_T(8, 12, 32, 64), DDB_T(2, 20, 8, 32),  DDB_T(4, 20, 8, 32),
     DDB_T(4, 20, 24, 64),
     DDB_T(8, 8, 32, 64),  DDB_T(16, 4, 48, 64),  DDB_TO(8, 4, 24, 32), DDB_TO(4, 4, 8, 32),

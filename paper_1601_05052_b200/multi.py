@@ -161,22 +161,42 @@ class ShardedDedisperser:
                 for c0, c1, ev in self.groups:
                     self.block[c0:c1, :t].copy_(host_block[c0:c1], non_blocking=True)
                     ev.record(self.h2d_stream)
-        last = len(self.groups) - 1
-        for gi, (c0, c1, ev) in enumerate(self.groups):
-            if len(self.groups) > 1:
-                self.stream.wait_event(ev)
-            for lo, hi, plan, done in self.chunks:
-                if len(self.groups) == 1:
-                    plan.execute(self.block.data_ptr(), self.out[lo].data_ptr())
-                else:
-                    plan.execute_channels(self.block.data_ptr(), self.out[lo].data_ptr(), c0, c1,
-                                          accumulate=gi > 0)
-                if gi == last:
-                    done.record(self.stream)
-                    with torch.cuda.stream(self.copy_stream):
-                        self.copy_stream.wait_event(done)
-                        host_out[lo:hi].copy_(self.out[lo:hi], non_blocking=True)
+        for gi, ci in self.launch_order():
+            c0, c1, ev = self.groups[gi]
+            lo, hi, plan, done = self.chunks[ci]
+            if len(self.groups) == 1:
+                plan.execute(self.block.data_ptr(), self.out[lo].data_ptr())
+            else:
+                self.stream.wait_event(ev)  # group gi's rows have landed
+                plan.execute_channels(self.block.data_ptr(), self.out[lo].data_ptr(), c0, c1,
+                                      accumulate=gi > 0)
+            if gi == len(self.groups) - 1:
+                done.record(self.stream)
+                with torch.cuda.stream(self.copy_stream):
+                    self.copy_stream.wait_event(done)
+                    host_out[lo:hi].copy_(self.out[lo:hi], non_blocking=True)
         self.copy_stream.synchronize()
+
+    def launch_order(self):
+        """(channel group, DM chunk) kernel order for run_host.  No chunk can
+        go D2H before the whole block is on the device, so the first
+        `lead` chunks run their leading channel groups while the later
+        groups are still in flight; after that each chunk is finished and
+        handed to the copy stream in turn, so the D2H of the output (the
+        larger transfer) starts as soon as the H2D ends.  Per output the
+        groups still run in ascending channel order (bit-exact)."""
+        n, g = len(self.chunks), len(self.groups)
+        lead = n if g == 1 else max(1, (n + 1) // 2)
+        order, done = [], set()
+        for gi in range(g - 1):
+            for ci in range(lead):
+                order.append((gi, ci))
+                done.add((gi, ci))
+        for ci in range(n):
+            for gi in range(g):
+                if (gi, ci) not in done:
+                    order.append((gi, ci))
+        return order
 
     def gather(self) -> Optional[torch.Tensor]:
         with torch.cuda.stream(self.stream):
