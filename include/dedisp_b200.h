@@ -91,6 +91,11 @@ typedef struct dd_config {
  * <= 4 consumer warps per CTA) when one exists for the shape; otherwise the
  * flag is ignored.  A tuning knob: occupancy against register pressure. */
 #define DD_CONFIG_HIGH_OCCUPANCY 0x2u
+/* Staged families: order the CTAs time-fastest instead of DM-fastest.  With
+ * large delays (LOFAR) DM-fastest resident CTAs read windows spread over the
+ * whole input block, which then streams from HBM once per time tile;
+ * time-fastest keeps the resident working set to one DM group's region. */
+#define DD_CONFIG_TIME_MAJOR 0x8u
 /* Staged families: channels per pipeline stage in bits 8..11 (1..15; 0 lets
  * the plan choose).  A tuning knob: larger stages amortise the per-stage
  * synchronisation, smaller ones leave shared memory for more CTAs per SM. */

@@ -374,8 +374,8 @@ dd_status dd_validate_config(const dd_config* k, uint32_t num_dms, uint32_t s,
     return fail(DD_ERR_INVALID_ARGUMENT, "work_time * work_dm exceeds the accumulator limit of " +
                                              std::to_string(L.max_accumulators));
   if (k->staging > DD_STAGING_TMEM) return fail(DD_ERR_INVALID_ARGUMENT, "unknown staging mode");
-  if (k->flags &
-      ~(DD_CONFIG_GPU_TILING | DD_CONFIG_HIGH_OCCUPANCY | DD_CONFIG_CPS_MASK | DD_CONFIG_NSTAGE_MASK))
+  if (k->flags & ~(DD_CONFIG_GPU_TILING | DD_CONFIG_HIGH_OCCUPANCY | DD_CONFIG_TIME_MAJOR |
+                   DD_CONFIG_CPS_MASK | DD_CONFIG_NSTAGE_MASK))
     return fail(DD_ERR_INVALID_ARGUMENT, "unknown config flags");
 
   const uint32_t ns = (k->flags & DD_CONFIG_NSTAGE_MASK) >> DD_CONFIG_NSTAGE_SHIFT;
@@ -595,6 +595,7 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
   a.out_beam_stride = 0;
   a.depth = std::max<uint32_t>(1, k->dm_tile_depth);
   a.depth = std::min(a.depth, a.tiles_dm);
+  a.time_major = (k->flags & DD_CONFIG_TIME_MAJOR) ? 1u : 0u;
 
   const uint64_t block = static_cast<uint64_t>(k->items_time) * k->items_dm;
   const bool smem_shape = smem_variant_ok(k->work_dm, k->work_time, block);

@@ -162,6 +162,7 @@ struct TiledArgs {
   uint32_t items_time, items_dm, work_time, work_dm;
   uint32_t tile_time, tile_dm, tiles_time, tiles_dm;
   uint32_t depth;      // DM tiles per CTA
+  uint32_t time_major; // staged families: CTA raster time-fastest (else DM-fastest)
   uint32_t win_cap;    // floats per staged channel window (multiple of 4)
   uint32_t rec_bytes;
   uint32_t cps;        // channels per pipeline stage

@@ -114,8 +114,16 @@ __device__ __forceinline__ Pipe pipe_setup(const TiledArgs& a, uint8_t* smem) {
   p.recs = smem + kPipeHeader;
   p.wins = reinterpret_cast<float*>(p.recs + a.nstage * a.cps * a.rec_bytes);
   const uint32_t groups_dm = (a.tiles_dm + a.depth - 1) / a.depth;
-  p.t0 = (blockIdx.x / groups_dm) * a.tile_time;
-  p.b_first = (blockIdx.x % groups_dm) * a.depth;
+  if (a.time_major) {
+    // time-fastest: the resident CTAs cover few DM groups over many time
+    // tiles, so their windows share one input region per DM group (for
+    // large delays, where DM-fastest CTAs touch the whole block at once)
+    p.t0 = (blockIdx.x % a.tiles_time) * a.tile_time;
+    p.b_first = (blockIdx.x / a.tiles_time) * a.depth;
+  } else {
+    p.t0 = (blockIdx.x / groups_dm) * a.tile_time;
+    p.b_first = (blockIdx.x % groups_dm) * a.depth;
+  }
   const uint32_t ntiles = min(a.depth, a.tiles_dm - p.b_first);
   p.nchunk = (a.ch_end - a.ch_begin + a.cps - 1) / a.cps;
   p.total = ntiles * p.nchunk;

@@ -255,7 +255,8 @@ def test_non_monotone_and_fault_injected_tables(dev, golden):
     ("tmem", K(32, 4, 4, 4), 4, "occ"), ("tmem", K(32, 4, 8, 4), 8, "occ"),
     ("tmem", K(32, 2, 12, 8), 3), ("tmem", K(32, 1, 12, 8), 1), ("tmem", K(32, 4, 20, 4), 2),
     ("tmem", K(32, 4, 12, 8), 15), ("tmem", K(32, 4, 12, 8), 11), ("smem", K(32, 4, 4, 4), 13),
-    ("regwin", K(32, 4, 12, 4), 15)])
+    ("regwin", K(32, 4, 12, 4), 15), ("tmem", K(32, 4, 12, 8), 15, "tm"),
+    ("smem", K(32, 4, 4, 4), 8, "tm"), ("regwin", K(32, 4, 12, 4), 4, "tm")])
 def test_gpu_tiling_predicated_tail(dev, golden, spec):
     """GPU-native tiles whose tile_time does not divide s (vector register
     windows, odd smem tiles, TMEM windows incl. the three-CTA builds): the
@@ -272,7 +273,8 @@ def test_gpu_tiling_predicated_tail(dev, golden, spec):
     out = torch.full((d, s), float("nan"), device="cuda")
     torch.cuda.synchronize()
     p = dev.plan(sh.data_ptr(), c, d, s, t, t, cfg, 1, staging, gpu_tiling=True,
-                 stage_channels=cps, high_occupancy=mode == "occ")
+                 stage_channels=cps, high_occupancy=mode == "occ",
+                 flags=N.DD_CONFIG_TIME_MAJOR if mode == "tm" else 0)
     info = p.info()
     assert info["family"] == staging and info["channels_per_stage"] == cps
     if mode == "occ":

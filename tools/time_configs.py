@@ -4,7 +4,7 @@
 
 Extra fields: "g" requests GPU tiling (tile_time need not divide s),
 "cpsN" pins N channels per pipeline stage, "occ" the TMEM three-CTA build,
-"nsN" N pipeline stages.
+"nsN" N pipeline stages, "tm" time-major CTA raster.
 """
 import os
 import sys
@@ -12,6 +12,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
+from paper_1601_05052_b200 import _native as N  # noqa: E402
 from paper_1601_05052_b200 import _native as N  # noqa: E402
 from paper_1601_05052_b200 import api  # noqa: E402
 
@@ -37,8 +38,9 @@ def main():
                          gpu_tiling="g" in extra,
                          stage_channels=next((int(x[3:]) for x in extra if x.startswith("cps")), 0),
                          high_occupancy="occ" in extra,
-                         flags=next((int(x[2:]) for x in extra if x.startswith("ns")), 0)
-                         << N.DD_CONFIG_NSTAGE_SHIFT)
+                         flags=(next((int(x[2:]) for x in extra if x.startswith("ns")), 0)
+                                << N.DD_CONFIG_NSTAGE_SHIFT)
+                         | (N.DD_CONFIG_TIME_MAJOR if "tm" in extra else 0))
         except ValueError as e:
             print(f"{spec:28s} invalid: {e}")
             continue
