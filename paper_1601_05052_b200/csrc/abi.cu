@@ -118,6 +118,7 @@ dd_status dd_context_create(int device, dd_context** out) {
   c->own_stream = true;
   c->sm_count = p.multiProcessorCount;
   c->smem_optin = static_cast<int>(p.sharedMemPerBlockOptin);
+  c->l2_bytes = p.l2CacheSize;
   c->cc_major = p.major;
   c->cc_minor = p.minor;
   if (p.major < 10)
@@ -596,6 +597,16 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
   a.depth = std::max<uint32_t>(1, k->dm_tile_depth);
   a.depth = std::min(a.depth, a.tiles_dm);
   a.time_major = (k->flags & DD_CONFIG_TIME_MAJOR) ? 1u : 0u;
+  if (k->staging == DD_STAGING_AUTO && !a.time_major) {
+    // AUTO also picks the raster: DM-fastest unless the windows of the
+    // CTAs resident at once (~2 per SM, one time tile, their DM range)
+    // would overflow 3/4 of the L2 -- large delays (LOFAR), where the block
+    // would otherwise stream from HBM once per time tile.
+    const double resident_dms = std::min<double>(
+        num_dms, 2.0 * c->sm_count * a.tile_dm * std::max<uint32_t>(1, a.depth));
+    const double window = a.tile_time + static_cast<double>(md) * resident_dms / num_dms;
+    if (4.0 * channels * window > 0.75 * c->l2_bytes) a.time_major = 1;
+  }
 
   const uint64_t block = static_cast<uint64_t>(k->items_time) * k->items_dm;
   const bool smem_shape = smem_variant_ok(k->work_dm, k->work_time, block);
@@ -656,7 +667,7 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
         fn = find_tmem_kernel(k->work_dm, k->work_time, p->group_span, &p->regwin_span);
       slack = p->regwin_span + 8;
     } else {
-      fn = find_smem_kernel(k->work_dm, k->work_time);
+      fn = find_smem_kernel(k->work_dm, k->work_time, nullptr, k->items_time);
     }
     uint32_t win_cap = 0, rec_bytes = 0, cps = 0, nstage = 0, smem = 0;
     // the launch must fit the variant's register budget

@@ -275,16 +275,19 @@ __device__ __forceinline__ void staged_loop(const TiledArgs& a, uint8_t* smem) {
 // conflict-free shared-memory wavefront per warp-load, one load per add.
 // Bound: shared-memory operand bandwidth (32 adds/clk/SM).
 // ---------------------------------------------------------------------
-template <int K, int W>
+template <int K, int W, int IT = 0>
 struct SmemBody {
   static constexpr bool kRowBase = false;  // channel() gets the row at lo's sample
   const TiledArgs& a;
   uint32_t it, id;
   float acc[K][W];
 
+  // IT > 0: items_time fixed at compile time, so a thread's W samples sit
+  // at immediate offsets from one address (no per-load address arithmetic)
+  __device__ __forceinline__ uint32_t stride() const { return IT > 0 ? IT : a.items_time; }
   __device__ SmemBody(const TiledArgs& args) : a(args) {
-    it = threadIdx.x % a.items_time;
-    id = threadIdx.x / a.items_time;
+    it = threadIdx.x % stride();
+    id = threadIdx.x / stride();
   }
   __device__ __forceinline__ void zero() {
 #pragma unroll
@@ -298,7 +301,7 @@ struct SmemBody {
     for (int k = 0; k < K; ++k) {
       const float* p = w + r[4 + id + k * a.items_dm];
 #pragma unroll
-      for (int j = 0; j < W; ++j) acc[k][j] += p[j * a.items_time];
+      for (int j = 0; j < W; ++j) acc[k][j] += p[j * stride()];
     }
   }
   __device__ __forceinline__ void load(uint32_t dm0, uint32_t t0) {
@@ -330,10 +333,10 @@ constexpr int smem_max_threads() {
   return K * W > 32 ? 256 : (K * W > 16 ? 512 : 992);
 }
 
-template <int K, int W>
+template <int K, int W, int IT = 0>
 __global__ void __launch_bounds__(smem_max_threads<K, W>() + 32) k_smem(const TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  staged_loop<SmemBody<K, W>>(a, smem);
+  staged_loop<SmemBody<K, W, IT>>(a, smem);
 }
 
 // ---------------------------------------------------------------------
@@ -811,12 +814,13 @@ __global__ void __launch_bounds__(160, 3) k_tmemwin_occ(const TiledArgs a) {
 using KernelFn = void (*)(const TiledArgs);
 
 struct SmemVariant {
-  int k, w;
+  int k, w, it;  // it = 0: items_time at run time
   KernelFn fn;
   int max_threads;
 };
 
-#define DDB_V(K, W) {K, W, k_smem<K, W>, smem_max_threads<K, W>()}
+#define DDB_V(K, W) {K, W, 0, k_smem<K, W>, smem_max_threads<K, W>()}
+#define DDB_VI(K, W, I) {K, W, I, k_smem<K, W, I>, smem_max_threads<K, W>()}
 static const SmemVariant kSmemVariants[] = {
     DDB_V(1, 1),  DDB_V(1, 2),  DDB_V(1, 4),  DDB_V(1, 5),  DDB_V(1, 8),  DDB_V(1, 10),
     DDB_V(1, 16), DDB_V(1, 25), DDB_V(2, 1),  DDB_V(2, 2),  DDB_V(2, 4),  DDB_V(2, 5),
@@ -824,16 +828,27 @@ static const SmemVariant kSmemVariants[] = {
     DDB_V(4, 4),  DDB_V(4, 5),  DDB_V(4, 8),  DDB_V(4, 10), DDB_V(4, 16), DDB_V(8, 1),
     DDB_V(8, 2),  DDB_V(8, 4),  DDB_V(8, 5),  DDB_V(8, 8),  DDB_V(16, 1), DDB_V(16, 2),
     DDB_V(16, 4),
+    // compile-time items_time for the shapes the sweeps select (tuning/)
+    DDB_VI(1, 5, 32), DDB_VI(2, 5, 32), DDB_VI(4, 5, 32), DDB_VI(1, 25, 8), DDB_VI(4, 10, 16),
+    DDB_VI(2, 5, 160), DDB_VI(1, 25, 64), DDB_VI(2, 25, 64), DDB_VI(4, 10, 160),
+    DDB_VI(2, 10, 160), DDB_VI(2, 25, 160),
 };
 #undef DDB_V
+#undef DDB_VI
 
-KernelFn find_smem_kernel(uint32_t k, uint32_t w, uint32_t* max_threads) {
-  for (const SmemVariant& v : kSmemVariants)
-    if (static_cast<uint32_t>(v.k) == k && static_cast<uint32_t>(v.w) == w) {
+KernelFn find_smem_kernel(uint32_t k, uint32_t w, uint32_t* max_threads, uint32_t items_time) {
+  const SmemVariant* generic = nullptr;
+  for (const SmemVariant& v : kSmemVariants) {
+    if (static_cast<uint32_t>(v.k) != k || static_cast<uint32_t>(v.w) != w) continue;
+    if (v.it == 0 && generic == nullptr) generic = &v;
+    if (items_time != 0 && static_cast<uint32_t>(v.it) == items_time) {
       if (max_threads) *max_threads = static_cast<uint32_t>(v.max_threads);
       return v.fn;
     }
-  return nullptr;
+  }
+  if (generic == nullptr) return nullptr;
+  if (max_threads) *max_threads = static_cast<uint32_t>(generic->max_threads);
+  return generic->fn;
 }
 
 struct RegWinVariant {

@@ -16,6 +16,7 @@ struct dd_context {
   bool own_stream = false;
   int sm_count = 0;
   int smem_optin = 0;
+  int l2_bytes = 0;
   int cc_major = 0, cc_minor = 0;
   uint32_t* d_scratch = nullptr;  // 4 x u32 reduction slots
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
@@ -56,7 +57,9 @@ cudaError_t launch_max_u32(const uint32_t* d_v, uint64_t n, uint32_t* d_out, cud
 using KernelFn = void (*)(const TiledArgs);
 // Staged-kernel variant for work_dm x work_time; nullptr when not
 // instantiated.  *max_threads = the variant's block-size cap.
-KernelFn find_smem_kernel(uint32_t k, uint32_t w, uint32_t* max_threads = nullptr);
+// items_time != 0 selects a compile-time-stride build when one exists
+KernelFn find_smem_kernel(uint32_t k, uint32_t w, uint32_t* max_threads = nullptr,
+                          uint32_t items_time = 0);
 // Register-window variant for (work_dm, work_time) covering group_span
 // (or the widest one); *span_out = its SPAN.  nullptr when not instantiated.
 KernelFn find_regwin_kernel(uint32_t k, uint32_t w, uint32_t group_span, uint32_t* span_out);

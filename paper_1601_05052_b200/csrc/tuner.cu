@@ -184,11 +184,14 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
     if (block < 64 || !smem_variant_ok(k.work_dm, k.work_time, block)) continue;
     for (uint32_t depth : {1u, 2u}) {
       if (depth > 1 && tiles_dm < depth * 2) continue;
-      for (uint32_t cps : {8u, 15u}) {
+      // 8 or 15 channels per stage; the time-major raster (large delays)
+      // with the wide stages
+      for (uint32_t flags : {8u << DD_CONFIG_CPS_SHIFT, 15u << DD_CONFIG_CPS_SHIFT,
+                             (15u << DD_CONFIG_CPS_SHIFT) | DD_CONFIG_TIME_MAJOR}) {
         dd_config c = k;
         c.dm_tile_depth = depth;
         c.staging = DD_STAGING_SMEM;
-        c.flags = cps << DD_CONFIG_CPS_SHIFT;
+        c.flags = flags;
         v.push_back(c);
       }
     }
