@@ -354,6 +354,8 @@ def run_ours(args):
                                   if cfg_src and cfg_src != "cli" else (cfg_src or "default")},
                 "kernel_family": info["family"], "smem_bytes": info["smem_bytes"],
                 "grid": info["grid_x"], "block": info["block_threads"],
+                "stages": info["stages"], "registers": info["registers"],
+                "cta_raster": "time-major" if info["time_major"] else "dm-major",
                 "parallelism": f"dm-shard x{world_size}",
                 "l2": f"flushed between timed steps ({args.flush_mb} MB memset outside the events)",
             },

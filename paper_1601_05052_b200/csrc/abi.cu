@@ -763,6 +763,7 @@ dd_status dd_plan_get_info(const dd_plan* p, dd_plan_info* info) {
   info->stages = p->args.nstage;
   info->kernel_launches = 1;
   info->staged_bytes = p->staged_bytes;
+  info->time_major = p->args.time_major;
   if (p->smem_fn != nullptr) {
     cudaFuncAttributes fa{};
     int ctas = 0;
