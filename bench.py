@@ -48,6 +48,7 @@ def parse():
     p.add_argument("--flush-mb", type=int, default=256)
     p.add_argument("--e2e-chunks", type=int, default=8)
     p.add_argument("--e2e-channel-groups", type=int, default=2)
+    p.add_argument("--e2e-h2d", default="auto", choices=["auto", "time", "channels"])
     return p.parse_args()
 
 
@@ -236,8 +237,7 @@ def run_ours(args):
         cfgt, cfg_src = tuned_config(setup.name, d)
     cfg = api.KernelConfig(*cfgt[:4])
     flags = cfgt[6]
-    dd = multi.ShardedDedisperser(setup, d, cfg, cfgt[4], cfgt[5], device=local,
-                                  gpu_tiling=bool(flags & 1), stage_channels=(flags >> 8) & 15)
+    dd = multi.ShardedDedisperser(setup, d, cfg, cfgt[4], cfgt[5], device=local, flags=flags)
     c, s, t = setup.channels, setup.samples_per_second, dd.num_samples
     stream = dd.stream
     torch.cuda.set_stream(stream)  # events, flushes and copies share the library's stream
@@ -289,7 +289,7 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         h_out = torch.empty((dd.count, s), dtype=torch.float32).pin_memory()
-        dd.pipeline(args.e2e_chunks, args.e2e_channel_groups)
+        dd.pipeline(args.e2e_chunks, args.e2e_channel_groups, args.e2e_h2d)
         e2e_ms = []
         for i in range(max(2, args.steps // 3) + 1):
             if world_size > 1:
@@ -309,11 +309,17 @@ def run_ours(args):
                "h2d_bytes_per_step": c * t * 4 if rank == 0 else 0,
                "d2h_bytes_per_step": d * s * 4,
                "dm_chunks": len(dd.chunks), "channel_groups": len(dd.groups),
-               "path": "pinned H2D of the [c][t] block by channel groups overlapped with the "
-                       "kernels of the groups already landed (accumulating through the output, "
-                       "bit-exact; with N>1: H2D on rank 0 + NCCL broadcast), and D2H of each "
-                       "DM chunk's rows overlapped with the remaining kernels; host-timed, "
-                       "synchronised at the end"}
+               "h2d_order": dd.h2d_mode,
+               "path": ("pinned H2D of the [c][t] block in time order (2-D copies, "
+                        "dd_upload_block_range), each DM chunk's kernel starting once the "
+                        "samples its delays reach have landed, and D2H of each chunk's rows "
+                        "overlapped with the remaining uploads and kernels"
+                        if dd.h2d_mode == "time" else
+                        "pinned H2D of the [c][t] block by channel groups overlapped with the "
+                        "kernels of the groups already landed (accumulating through the output, "
+                        "bit-exact; with N>1: H2D on rank 0 + NCCL broadcast), and D2H of each "
+                        "DM chunk's rows overlapped with the remaining kernels")
+                       + "; host-timed, synchronised at the end"}
 
     cpu = None
     if rank == 0 and world_size == 1 and not args.no_cpu:

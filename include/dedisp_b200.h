@@ -274,6 +274,17 @@ dd_status dd_sigproc_to_filterbank(dd_context* ctx, const float* d_payload, uint
                                    uint64_t num_samples, float* d_dst, uint64_t dst_pitch,
                                    int64_t* first_bad);
 
+/* Streaming upload: samples [t0, t1) of every channel of a host filterbank
+ * block (row pitch h_pitch floats; pinned memory for an asynchronous copy)
+ * into the device block (row pitch d_pitch floats), as one 2-D copy enqueued
+ * on `stream` (a cudaStream_t; NULL = the context stream).  Lets a caller
+ * ship a block in time order, so the DMs whose delays fit the first part can
+ * start -- and their output leave the device -- before the block's tail
+ * lands. */
+dd_status dd_upload_block_range(dd_context* ctx, const float* h_block, uint64_t h_pitch,
+                                float* d_block, uint64_t d_pitch, uint32_t channels,
+                                uint64_t t0, uint64_t t1, void* stream);
+
 /* ---------------------------------------------- synthetic input ------- */
 /* noise_filterbank, filterbank.cpp:60-80: mt19937_64(seed), Box-Muller,
  * channel-major fill, float(sigma * g).  Host memory; threads = 0 -> all. */

@@ -128,6 +128,7 @@ SIGNATURES = {
                             C.POINTER(dd_limits), P]),
     "dd_noise_filterbank": (i32, [u32, u64, C.c_float, u64, C.c_int, P]),
     "dd_sigproc_to_filterbank": (i32, [P, P, u32, u64, P, u64, C.POINTER(C.c_int64)]),
+    "dd_upload_block_range": (i32, [P, P, u64, P, u64, u32, u64, u64, P]),
     "dd_enumerate_configs": (i32, [u32, u32, C.POINTER(dd_limits), C.POINTER(dd_config), u64, pu64]),
     "dd_enumerate_gpu_configs": (i32, [P, C.POINTER(dd_setup), u32, C.POINTER(dd_limits),
                                        C.POINTER(dd_config), u64, pu64]),

@@ -384,6 +384,14 @@ class Context:
                                              C.byref(bad)))
         return bad.value
 
+    def upload_block_range(self, h_block: int, h_pitch: int, d_block: int, d_pitch: int,
+                           channels: int, t0: int, t1: int, stream: int = 0) -> None:
+        """Samples [t0, t1) of every channel, host -> device, one async 2-D
+        copy on `stream` (a cudaStream_t; 0 = the context stream)."""
+        check(lib().dd_upload_block_range(self.handle, C.c_void_p(h_block), h_pitch,
+                                          C.c_void_p(d_block), d_pitch, channels, t0, t1,
+                                          C.c_void_p(stream)))
+
     def plan(self, d_shifts: int, channels: int, num_dms: int, samples_per_second: int,
              num_samples: int, in_pitch: int, cfg: Optional[KernelConfig] = None,
              dm_tile_depth: int = 1, staging: str = "auto",

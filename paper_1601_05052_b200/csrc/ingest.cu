@@ -73,3 +73,18 @@ extern "C" dd_status dd_sigproc_to_filterbank(dd_context* c, const float* d_payl
   if (first_bad) *first_bad = h == ~0ull ? -1 : static_cast<int64_t>(h);
   return DD_OK;
 }
+
+extern "C" dd_status dd_upload_block_range(dd_context* c, const float* h_block, uint64_t h_pitch,
+                                           float* d_block, uint64_t d_pitch, uint32_t channels,
+                                           uint64_t t0, uint64_t t1, void* stream) {
+  if (c == nullptr || h_block == nullptr || d_block == nullptr)
+    return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  if (t1 < t0 || t1 > h_pitch || t1 > d_pitch)
+    return fail(DD_ERR_INVALID_ARGUMENT, "sample range outside the block");
+  if (t1 == t0 || channels == 0) return DD_OK;
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+  const cudaError_t e = cudaMemcpy2DAsync(d_block + t0, d_pitch * 4, h_block + t0, h_pitch * 4,
+                                          (t1 - t0) * 4, channels, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "dd_upload_block_range");
+  return DD_OK;
+}

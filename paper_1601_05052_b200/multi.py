@@ -78,7 +78,9 @@ class ShardedDedisperser:
 
     def __init__(self, setup: api.ObservationSetup, num_dms: int, cfg: api.KernelConfig,
                  dm_tile_depth: int = 1, staging: str = "auto", device: Optional[int] = None,
-                 gpu_tiling: bool = False, stage_channels: int = 0):
+                 gpu_tiling: bool = False, stage_channels: int = 0, flags: int = 0):
+        """flags: raw DD_CONFIG_* bits (as in tuning records), OR-ed with the
+        gpu_tiling / stage_channels arguments."""
         self.rank, self.world = world()
         self.setup, self.num_dms, self.cfg = setup, num_dms, cfg
         self.device = torch.cuda.current_device() if device is None else device
@@ -98,11 +100,12 @@ class ShardedDedisperser:
                                               dm_offset=self.offset)
         self.block = torch.empty((c, self.pitch), dtype=torch.float32, device=self.device)
         self.out = torch.empty((self.count, s), dtype=torch.float32, device=self.device)
-        self._depth, self._staging, self._gpu_tiling, self._cps = (dm_tile_depth, staging,
-                                                                   gpu_tiling, stage_channels)
+        self._depth, self._staging, self._gpu_tiling, self._cps, self._flags = (
+            dm_tile_depth, staging, gpu_tiling, stage_channels, flags)
         self.plan = self.ctx.plan(self.shifts.data_ptr(), c, self.count, s, self.num_samples,
                                   self.pitch, cfg, dm_tile_depth, staging,
-                                  gpu_tiling=gpu_tiling, stage_channels=stage_channels)
+                                  gpu_tiling=gpu_tiling, stage_channels=stage_channels,
+                                  flags=flags)
 
     @property
     def flop(self) -> int:
@@ -122,13 +125,17 @@ class ShardedDedisperser:
         self.plan.execute(self.block.data_ptr(), self.out.data_ptr())
         return self.out
 
-    def pipeline(self, chunks: int, channel_groups: int = 4) -> None:
+    def pipeline(self, chunks: int, channel_groups: int = 4, h2d: str = "auto") -> None:
         """Prepare run_host(): the shard's DM range cut into `chunks` plans
         (tile-aligned), each over its slice of the shift table, so the D2H of
-        chunk i overlaps the kernel of chunk i+1; and (single rank, staged
-        families) the channel axis cut into `channel_groups` so the H2D of
-        group g+1 overlaps the kernels of group g (accumulating through the
-        output, bit-exact)."""
+        chunk i overlaps the kernel of chunk i+1.  The block goes H2D either
+        in time order (h2d="time"; single rank): chunk i starts once the
+        samples its delays reach have landed -- the low-DM chunks need little
+        more than the first second -- so output leaves the device while the
+        block's tail is still arriving; or (h2d="channels"; staged families)
+        in `channel_groups` channel ranges, the kernels of group g
+        accumulating through the output (bit-exact) under the H2D of group
+        g+1.  "auto": time order on a single rank."""
         c, s, td = self.setup.channels, self.setup.samples_per_second, self.cfg.tile_dm()
         units = self.count // td
         chunks = max(1, min(chunks, units))
@@ -139,10 +146,26 @@ class ShardedDedisperser:
             plan = self.ctx.plan(self.shifts.data_ptr() + lo * c * 4, c, hi - lo, s,
                                  self.num_samples, self.pitch, self.cfg, self._depth,
                                  self._staging, gpu_tiling=self._gpu_tiling,
-                                 stage_channels=self._cps)
+                                 stage_channels=self._cps, flags=self._flags)
             self.chunks.append((lo, hi, plan, torch.cuda.Event()))
         staged = self.chunks[0][2].info()["family"] in ("smem", "regwin", "tmem")
-        g = max(1, min(channel_groups, c)) if (staged and self.world == 1) else 1
+        self.h2d_mode = h2d if h2d != "auto" else ("time" if self.world == 1 else "channels")
+        if self.world > 1:
+            self.h2d_mode = "channels"
+        if self.h2d_mode == "time":
+            # samples chunk i may read: its largest shift + s, plus one tile of
+            # slack for a predicated last tile and the 16-byte copy rounding
+            # (chunks are cut in DM order; the running maximum keeps the
+            # uploads in time order for any table)
+            tt = self.cfg.tile_time()
+            self.uploads, upto = [], 0
+            for lo, hi, _, _ in self.chunks:
+                md = int(self.shifts[lo:hi].max().item())
+                upto = max(upto, min(self.num_samples, s + md + tt + 8))
+                self.uploads.append((upto, torch.cuda.Event()))
+            g = 1
+        else:
+            g = max(1, min(channel_groups, c)) if (staged and self.world == 1) else 1
         self.groups = [(c * i // g, c * (i + 1) // g, torch.cuda.Event()) for i in range(g)]
         self.h2d_stream = torch.cuda.Stream(self.device)
         self.copy_stream = torch.cuda.Stream(self.device)
@@ -154,6 +177,26 @@ class ShardedDedisperser:
         chunk's output rows go D2H as soon as its last kernel is done.
         host_out: pinned [count][s]."""
         t = self.num_samples
+        if self.h2d_mode == "time":
+            with torch.cuda.stream(self.h2d_stream):
+                done_t = 0
+                for upto, ev in self.uploads:
+                    if upto > done_t:
+                        self.ctx.upload_block_range(host_block.data_ptr(), t,
+                                                    self.block.data_ptr(), self.pitch,
+                                                    self.setup.channels, done_t, upto,
+                                                    self.h2d_stream.cuda_stream)
+                        done_t = upto
+                    ev.record(self.h2d_stream)
+            for (lo, hi, plan, done), (_, ev) in zip(self.chunks, self.uploads):
+                self.stream.wait_event(ev)  # the samples this chunk reads have landed
+                plan.execute(self.block.data_ptr(), self.out[lo].data_ptr())
+                done.record(self.stream)
+                with torch.cuda.stream(self.copy_stream):
+                    self.copy_stream.wait_event(done)
+                    host_out[lo:hi].copy_(self.out[lo:hi], non_blocking=True)
+            self.copy_stream.synchronize()
+            return
         if len(self.groups) == 1:
             self.load(host_block)
         else:

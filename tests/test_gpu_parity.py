@@ -378,10 +378,21 @@ def test_sharded_driver_host_pipeline(dev, golden):
     setup, table, fb = _golden_instance(g)
     dd = multi.ShardedDedisperser(setup, g["num_dms"], K(16, 8, 10, 4), 1, "smem", device=0,
                                   stage_channels=8)
-    dd.pipeline(3, 4)
+    dd.pipeline(3, 4, h2d="channels")
     assert len(dd.groups) == 4
     host = torch.from_numpy(fb.data).pin_memory()
     out = torch.empty((dd.count, setup.samples_per_second), dtype=torch.float32).pin_memory()
+    dd.run_host(host, out)
+    torch.cuda.synchronize()
+    assert O.fnv1a(out.numpy()) == g["out_fnv"]
+    # time-ordered H2D (dd_upload_block_range): low-DM chunks start on a
+    # prefix of the block; the uploads cover the whole block by the end
+    dd.block.fill_(float("nan"))
+    out.zero_()
+    dd.pipeline(5, h2d="time")
+    assert dd.h2d_mode == "time"
+    ups = [u for u, _ in dd.uploads]
+    assert ups == sorted(ups) and ups[0] < dd.num_samples and ups[-1] <= dd.num_samples
     dd.run_host(host, out)
     torch.cuda.synchronize()
     assert O.fnv1a(out.numpy()) == g["out_fnv"]
