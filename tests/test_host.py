@@ -47,6 +47,21 @@ def test_no_device_fails_loudly():
         api.Context(0)
 
 
+def test_argument_errors_need_no_device():
+    """Argument checks run before any device work (and name the problem)."""
+    L = N.lib()
+    assert L.dd_upload_block_range(None, None, 0, None, 0, 1, 0, 1, None) == \
+        N.DD_ERR_INVALID_ARGUMENT
+    assert L.dd_plan_get_info(None, None) == N.DD_ERR_INVALID_ARGUMENT
+    bad = N.dd_config(32, 4, 5, 8, 1, N.STAGING["smem"], 1 << N.DD_CONFIG_NSTAGE_SHIFT)
+    assert L.dd_validate_config(C.byref(bad), 4096, 20000, None) == N.DD_ERR_INVALID_ARGUMENT
+    assert "stages" in L.dd_last_error().decode()
+    ok = N.dd_config(32, 4, 5, 8, 1, N.STAGING["tmem"],
+                     N.DD_CONFIG_TIME_MAJOR | (15 << N.DD_CONFIG_CPS_SHIFT)
+                     | (3 << N.DD_CONFIG_NSTAGE_SHIFT))
+    assert L.dd_validate_config(C.byref(ok), 4096, 20000, None) == N.DD_OK
+
+
 def test_geometry_known_answers(golden):
     # test_setup.cpp:15-24, :130-137
     assert math.isclose(api.delay_seconds(0.25, 1420.0, 1720.0), 1.63834524e-4, rel_tol=1e-8)
