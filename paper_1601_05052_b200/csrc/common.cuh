@@ -23,12 +23,6 @@ __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
 // Raise the phase's expected transaction bytes without arriving.
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
@@ -52,27 +46,15 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
-// 16-byte shared load under a predicate; the destination keeps its old
-// contents when the predicate is off (no zero-fill instructions).
-// As lds128_if, but the destination's previous value is declared dead: with
-// the predicate off the registers hold unspecified values.  For staging
-// buffers whose unloaded tail is never read, this lets the register
-// allocator reuse them between uses (the "+f" form keeps them live).
+// 16-byte shared load under a predicate, the destination's previous value
+// declared dead: with the predicate off the registers hold unspecified
+// values (for staging buffers whose unloaded tail is never read).
 __device__ __forceinline__ void lds128_maybe(bool pred, const float* addr, float& x, float& y,
                                              float& z, float& w) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
       "@q ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n\t}"
       : "=f"(x), "=f"(y), "=f"(z), "=f"(w)
-      : "r"(smem_addr(addr)), "r"(static_cast<int>(pred)));
-}
-
-__device__ __forceinline__ void lds128_if(bool pred, const float* addr, float& x, float& y,
-                                          float& z, float& w) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
-      "@q ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n\t}"
-      : "+f"(x), "+f"(y), "+f"(z), "+f"(w)
       : "r"(smem_addr(addr)), "r"(static_cast<int>(pred)));
 }
 

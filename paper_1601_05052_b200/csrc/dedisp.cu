@@ -194,17 +194,6 @@ __device__ __forceinline__ void pipe_produce(const TiledArgs& a, const Pipe& p) 
   }
 }
 
-__device__ __forceinline__ void pipe_init(const TiledArgs& a, const Pipe& p, uint32_t consumers) {
-  if (threadIdx.x == 0) {
-    for (uint32_t s = 0; s < a.nstage; ++s) {
-      mbar_init(&p.full[s], 1);
-      mbar_init(&p.empty[s], consumers);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-}
-
 // Warp-specialised pipeline.  The LAST warp of the CTA is the producer: one
 // lane runs ahead issuing bulk copies as soon as a slot is handed back
 // (empty[slot]), so the plan-record reads and copy latency stay off the
@@ -529,9 +518,6 @@ __global__ void __maxnreg__((regwin_maxreg<K, W, SPAN>())) k_regwin(const TiledA
 // issue as FADD2 (add.rn.f32x2: two independent IEEE RN adds).  Bit-exact:
 // every output still gets one add per channel, channels ascending.
 // ---------------------------------------------------------------------
-template <int N>
-struct TmemShape;
-
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
