@@ -431,7 +431,9 @@ def test_channel_range_passes_are_bit_identical(dev, golden, staging, cfg, tilin
 
 
 @pytest.mark.parametrize("staging,cfg,tiling", [("smem", K(16, 8, 10, 4), False),
-                                                ("tmem", K(32, 4, 12, 8), True)])
+                                                ("tmem", K(32, 4, 12, 8), True),
+                                                ("tm-smem", K(16, 8, 10, 4), False),
+                                                ("tm-tmem", K(32, 4, 12, 8), True)])
 def test_beam_batching(dev, staging, cfg, tiling):
     """dd_plan_execute_beams: B independent beams in one launch equal B single
     passes (each checked against the oracle on a DM subset)."""
@@ -445,7 +447,10 @@ def test_beam_batching(dev, staging, cfg, tiling):
     sh = torch.from_numpy(table.shifts.view(np.int32)).cuda()
     out = torch.full((beams, d, s), float("nan"), device="cuda")
     torch.cuda.synchronize()
-    p = dev.plan(sh.data_ptr(), c, d, s, t, t, cfg, 1, staging, gpu_tiling=tiling)
+    tm = staging.startswith("tm-")
+    p = dev.plan(sh.data_ptr(), c, d, s, t, t, cfg, 1, staging.replace("tm-", ""),
+                 gpu_tiling=tiling, flags=N.DD_CONFIG_TIME_MAJOR if tm else 0)
+    assert p.info()["time_major"] == int(tm)
     p.execute_beams(beams, x.data_ptr(), c * t, out.data_ptr(), d * s)
     dev.synchronize()
     got = out.cpu().numpy()
@@ -501,3 +506,43 @@ def test_sigproc_transpose_on_device(dev):
     src = torch.from_numpy(payload).cuda()
     torch.cuda.synchronize()
     assert dev.sigproc_to_filterbank(src.data_ptr(), c, t, dst.data_ptr(), pitch) == 500 * c + 3
+
+
+@pytest.mark.parametrize("flags", [0, "tm", "tm-ns2", "cps3-ns4"])
+def test_large_delay_instance_all_rasters(dev, flags):
+    """LOFAR-shaped delays (hundreds of samples per DM step, a block several
+    seconds long): every CTA raster and stage shape, including channel-range
+    passes accumulating through the output, reproduces the reference."""
+    import torch
+    setup = api.ObservationSetup("lofarish", 2000, 16, 138.0, 0.19, 0.0, 25.0)
+    d = 64
+    table = api.build_delay_table(setup, d)
+    t = api.instance_sizing(setup, d).num_samples
+    s, c = setup.samples_per_second, setup.channels
+    assert table.max_delay > 4 * s
+    fb = api.noise_filterbank(setup, t, 1.0, 33)
+    ref = O.dedisperse_reference(fb.data, table.shifts, s)
+    f = 0
+    if "tm" in str(flags):
+        f |= N.DD_CONFIG_TIME_MAJOR
+    if "ns2" in str(flags):
+        f |= 2 << N.DD_CONFIG_NSTAGE_SHIFT
+    if "cps3" in str(flags):
+        f |= (3 << N.DD_CONFIG_CPS_SHIFT) | (4 << N.DD_CONFIG_NSTAGE_SHIFT)
+    x = torch.from_numpy(fb.data).cuda()
+    sh = torch.from_numpy(table.shifts.view(np.int32)).cuda()
+    for cfg, depth in ((K(16, 4, 25, 1), 2), (K(40, 1, 10, 4), 1), (K(25, 2, 8, 2), 1)):
+        out = torch.full((d, s), float("nan"), device="cuda")
+        torch.cuda.synchronize()
+        p = dev.plan(sh.data_ptr(), c, d, s, t, t, cfg, depth, "smem", flags=f)
+        p.execute(x.data_ptr(), out.data_ptr())
+        dev.synchronize()
+        assert np.array_equal(_bits(out.cpu().numpy()), _bits(ref)), (cfg, flags)
+        out.fill_(float("nan"))
+        for i, (c0, c1) in enumerate([(0, 5), (5, 6), (6, 16)]):
+            p.execute_channels(x.data_ptr(), out.data_ptr(), c0, c1, accumulate=i > 0)
+        dev.synchronize()
+        assert np.array_equal(_bits(out.cpu().numpy()), _bits(ref)), (cfg, flags, "channels")
+    # the drop-in (AUTO) path on the same instance
+    got = api.dedisperse_tiled(fb, table, K(40, 1, 10, 4))
+    assert np.array_equal(_bits(got.data), _bits(ref))
