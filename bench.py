@@ -61,6 +61,21 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def onchip_ceilings(gflops, clocks):
+    """The on-chip ceilings the staged kernels are judged against (DESIGN.md
+    §3): one fp32 add per (output, channel) at 128 FP32 lanes/clk/SM, and one
+    4-byte shared-memory operand per add at 128 B/clk/SM, at the SM clock
+    sampled under load (max clock if no sample)."""
+    import torch
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz") or 1965.0
+    fp32 = sms * 128 * mhz * 1e6 / 1e9
+    lds = sms * 32 * mhz * 1e6 / 1e9
+    return {"sm_count": sms, "sm_mhz": mhz,
+            "fp32_add_gflops": round(fp32, 1), "frac_fp32_add": round(gflops / fp32, 4),
+            "smem_operand_gflops": round(lds, 1), "frac_smem_operand": round(gflops / lds, 4)}
+
+
 def tuned_config(setup_name, d):
     from paper_1601_05052_b200 import api
     path = os.path.join(ROOT, "tuning", f"{setup_name.lower()}_{d}.json")
@@ -372,6 +387,7 @@ def run_ours(args):
                          "peak_source": src,
                          "definition": "achieved = 4*(d*s*c + d*s + d*c) no-reuse bytes (Eq. 2) "
                                        "per launch / CUDA-event launch time"},
+            "onchip_ceilings": onchip_ceilings(value, cs),
             "gpu_launches": args.steps,
             "e2e": e2e,
             "cpu_baseline": cpu,
