@@ -579,6 +579,11 @@ struct TmemBody {
   static_assert(W + SPAN + 3 <= COLS, "window must fit the warp's TMEM columns");
   static_assert(K % 2 == 0, "DMs are read back in pairs");
   static constexpr bool kFullHead = FULL_HEAD;
+  // head vectors loaded unconditionally; the last one only when the window
+  // reaches it (measured: 8 always 6.68 ms, 7 + 1 predicated 6.53, 6 + 2
+  // 6.56 at Apertif d=4096 -- the predicated vector saves shared-memory
+  // bandwidth, but each predicated register stays live across the channel)
+  static constexpr int kHeadAlways = 7;
   // window columns beyond the first 32: 0, 8, 16 or 32
   static constexpr int kNeed = W + SPAN + 3 - 32;
   static constexpr int kTail = kNeed <= 0 ? 0 : kNeed <= 8 ? 8 : kNeed <= 16 ? 16 : 32;
@@ -639,12 +644,17 @@ struct TmemBody {
     n.base = w + col + g.y;  // w: the channel's 16-byte aligned row (kRowBase)
     const float* pa = n.base;
     if constexpr (kFullHead) {
-      // all 8 head vectors, unpredicated: columns past the window are never
-      // read back, the slot's slack keeps the reads inside shared memory,
-      // and unconditional definitions let the allocator retire the staging
+      // head vectors unpredicated: columns past the window are never read
+      // back, the slot's slack keeps the reads inside shared memory, and
+      // unconditional definitions let the allocator retire the staging
       // registers between channels (predicated ones keep them live)
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
+        if (i >= kHeadAlways) {
+          lds128_maybe(static_cast<uint32_t>(i) < n.nv, pa + 4 * i, n.win[4 * i],
+                       n.win[4 * i + 1], n.win[4 * i + 2], n.win[4 * i + 3]);
+          continue;
+        }
         const float4 v = *reinterpret_cast<const float4*>(pa + 4 * i);
         n.win[4 * i] = v.x;
         n.win[4 * i + 1] = v.y;
