@@ -681,10 +681,11 @@ struct TmemBody {
         // reuse the head's registers once the x32 store has read them
         const float* pa = n.base + 32;
         float* hi = n.win;
+        // nv > 8: the first tail vector is always needed
 #pragma unroll
         for (int i = 0; i < kTail / 4; ++i)
-          lds128_maybe(static_cast<uint32_t>(i) < n.nv - 8, pa + 4 * i, hi[4 * i], hi[4 * i + 1],
-                    hi[4 * i + 2], hi[4 * i + 3]);
+          lds128_maybe(i == 0 || static_cast<uint32_t>(i) < n.nv - 8, pa + 4 * i, hi[4 * i],
+                       hi[4 * i + 1], hi[4 * i + 2], hi[4 * i + 3]);
         if constexpr (kTail == 8) tmem_st8(taddr + 32, hi);
         else if constexpr (kTail == 16) tmem_st16(taddr + 32, hi);
         else tmem_st32(taddr + 32, hi);
