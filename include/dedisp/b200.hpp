@@ -285,4 +285,37 @@ MemoryTraffic kernel_traffic(const DelayTable& table, const KernelConfig& cfg,
 double measured_ai(std::uint64_t flops, const MemoryTraffic& traffic);
 double realtime_threshold_gflops(const ObservationSetup& setup, std::uint32_t num_dms);
 
+// analysis.hpp:43-58: devices covering `beams` beams in real time given one
+// pass's measured time (throws not_real_time_error for passes >= 1 s).
+struct DeploymentPlan {
+  std::uint32_t beams_per_device = 0;
+  std::uint64_t devices = 0;
+};
+DeploymentPlan deployment_sizing(const ObservationSetup& setup, std::uint32_t num_dms,
+                                 std::uint32_t beams, double measured_time_per_pass);
+
+// analysis.hpp:60-82: published peaks of the paper's five cards and the
+// roofline placement of an arithmetic intensity.
+struct DevicePeaks {
+  std::string name;
+  double peak_gflops = 0.0;
+  double peak_gbs = 0.0;
+  double ridge_flop_per_byte() const { return peak_gflops / peak_gbs; }
+};
+std::span<const DevicePeaks> reference_devices();
+struct RooflineVerdict {
+  bool memory_bound = false;
+  double ridge_flop_per_byte = 0.0;
+  double attainable_gflops = 0.0;
+};
+RooflineVerdict classify_roofline(double ai_flop_per_byte, double peak_gflops, double peak_gbs);
+
+// tuner.hpp:115-123: equal-width gflops histogram over [min, max].
+struct HistogramBin {
+  double lo = 0.0;
+  double hi = 0.0;
+  std::size_t count = 0;
+};
+std::vector<HistogramBin> make_histogram(const TuningResult& result, std::size_t bins);
+
 }  // namespace dedisp

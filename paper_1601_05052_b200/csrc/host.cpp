@@ -486,4 +486,65 @@ double realtime_threshold_gflops(const ObservationSetup& setup, std::uint32_t nu
   return static_cast<double>(num_dms) * setup.samples_per_second * setup.channels / 1e9;
 }
 
+DeploymentPlan deployment_sizing(const ObservationSetup& setup, std::uint32_t num_dms,
+                                 std::uint32_t beams, double t) {
+  setup.validate();
+  if (num_dms == 0) throw std::invalid_argument("need at least one trial DM");
+  if (beams == 0) throw std::invalid_argument("need at least one beam");
+  if (!std::isfinite(t) || t <= 0.0)
+    throw std::invalid_argument("pass time must be a positive number of seconds");
+  if (t >= 1.0)
+    throw not_real_time_error("one pass takes " + std::to_string(t) +
+                              " s; a device cannot keep up with even a single beam");
+  DeploymentPlan plan;
+  plan.beams_per_device = static_cast<std::uint32_t>(1.0 / t);
+  plan.devices = (static_cast<std::uint64_t>(beams) + plan.beams_per_device - 1) / plan.beams_per_device;
+  return plan;
+}
+
+std::span<const DevicePeaks> reference_devices() {
+  // the paper's Table 1 cards (GFLOP/s, GB/s)
+  static const DevicePeaks kDevices[] = {
+      {"AMD HD7970", 3788.0, 264.0},        {"Intel Xeon Phi 5110P", 2022.0, 320.0},
+      {"NVIDIA GTX 680", 3090.0, 192.0},    {"NVIDIA K20", 3519.0, 208.0},
+      {"NVIDIA GTX Titan", 4500.0, 288.0},
+  };
+  return kDevices;
+}
+
+RooflineVerdict classify_roofline(double ai, double peak_gflops, double peak_gbs) {
+  if (!std::isfinite(ai) || ai <= 0.0)
+    throw std::invalid_argument("arithmetic intensity must be positive");
+  if (!std::isfinite(peak_gflops) || peak_gflops <= 0.0 || !std::isfinite(peak_gbs) ||
+      peak_gbs <= 0.0)
+    throw std::invalid_argument("device peaks must be positive");
+  RooflineVerdict v;
+  v.ridge_flop_per_byte = peak_gflops / peak_gbs;
+  v.memory_bound = ai < v.ridge_flop_per_byte;
+  v.attainable_gflops = std::min(peak_gflops, ai * peak_gbs);
+  return v;
+}
+
+std::vector<HistogramBin> make_histogram(const TuningResult& result, std::size_t bins) {
+  if (bins == 0) throw std::invalid_argument("need at least one histogram bin");
+  if (result.records.empty()) throw std::invalid_argument("no records to bin");
+  double lo = result.records.front().gflops, hi = lo;
+  for (const TuningRecord& r : result.records) {
+    lo = std::min(lo, r.gflops);
+    hi = std::max(hi, r.gflops);
+  }
+  const double width = (hi - lo) / static_cast<double>(bins);
+  std::vector<HistogramBin> h(bins);
+  for (std::size_t i = 0; i < bins; ++i) {
+    h[i].lo = lo + width * static_cast<double>(i);
+    h[i].hi = i + 1 == bins ? hi : lo + width * static_cast<double>(i + 1);
+  }
+  for (const TuningRecord& r : result.records) {
+    std::size_t i = 0;  // a flat population lands in the first bin
+    if (width > 0.0) i = std::min(static_cast<std::size_t>((r.gflops - lo) / width), bins - 1);
+    ++h[i].count;
+  }
+  return h;
+}
+
 }  // namespace dedisp

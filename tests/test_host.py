@@ -224,3 +224,19 @@ def test_cxx_dropin_header_compiles_and_links(tmp_path):
                         "-ldedisp_b200", "-L", os.path.join(ROOT, "oracle"), "-loracle",
                         "-o", exe], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_cxx_analysis_layer(tmp_path):
+    """The reference's analysis/tuner helpers through the C++ drop-in header
+    (deployment sizing, device table, roofline, histogram): host-only, so it
+    runs here."""
+    import subprocess
+    exe = str(tmp_path / "analysis")
+    pkg = os.path.join(ROOT, "paper_1601_05052_b200")
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cxx", "test_analysis.cpp"), "-L", pkg,
+                        "-ldedisp_b200", "-Wl,-rpath," + pkg, "-o", exe],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "analysis: ok" in r.stdout, r.stdout + r.stderr
