@@ -11,6 +11,8 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
+# DDB_LIB: load another build of the same library (A/B kernel timing with
+# tools/time_configs.py); it must export every symbol below, no fallback.
 LIB_PATH = os.environ.get("DDB_LIB") or os.path.join(PKG, "libdedisp_b200.so")
 
 DD_OK, DD_ERR_INVALID_ARGUMENT, DD_ERR_CAPACITY, DD_ERR_CUDA, DD_ERR_NO_DEVICE, DD_ERR_INTERNAL = range(6)
