@@ -211,7 +211,9 @@ typedef struct dd_plan_info {
   uint32_t kernel_launches; /* launches per dd_plan_execute */
   uint64_t staged_bytes;  /* L2->SMEM bytes per execute (0 for direct) */
   uint32_t registers;     /* per thread, of the tiled kernel (0 otherwise) */
-  uint32_t ctas_per_sm;   /* resident CTAs per SM (occupancy API; 0 otherwise) */
+  uint32_t ctas_per_sm;   /* resident CTAs per SM by the occupancy API (0 if not
+                           * staged); conservative for the tcgen05 (TMEM) kernels,
+                           * which it reports as 1 while two run (ncu: ~10 warps/SM) */
   uint32_t time_major;    /* CTA raster time-fastest (DD_CONFIG_TIME_MAJOR or AUTO's pick) */
 } dd_plan_info;
 dd_status dd_plan_get_info(const dd_plan* plan, dd_plan_info* info);
