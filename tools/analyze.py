@@ -130,7 +130,8 @@ def main():
     a = p.parse_args()
     paths = [q for pat in a.results for q in sorted(glob.glob(pat)) or [pat]]
     paths = [q for q in paths if not q.endswith("_summary.json")]
-    results = [api.tuning_result_from_json(open(q).read()) for q in paths]
+    results = sorted((api.tuning_result_from_json(open(q).read()) for q in paths),
+                     key=lambda r: (r.zero_dm, r.num_dms))
     doc, csv = analyze(results, parse_roofline(a.roofline) if a.roofline else None, a.beams,
                        a.pass_time)
     os.makedirs(a.out, exist_ok=True)
