@@ -46,7 +46,10 @@ def main(rep):
             "smsp__issue_active.avg.pct_of_peak_sustained_active",
             "sm__inst_executed_pipe_fma.sum.pct_of_peak_sustained_active",
             "sm__warps_active.avg.per_cycle_active", "launch__registers_per_thread",
-            "lts__t_bytes.sum", "smsp__inst_executed.sum")
+            "lts__t_bytes.sum", "smsp__inst_executed.sum",
+            # L2 -> SM traffic (the TMA window staging) and L2 sector load
+            "l1tex__m_xbar2l1tex_read_bytes.sum", "l1tex__m_xbar2l1tex_read_bytes.sum.per_second",
+            "lts__t_sectors.sum.pct_of_peak_sustained_elapsed")
     print("metrics:")
     for i, n in enumerate(names):
         if n in keep:
