@@ -546,3 +546,34 @@ def test_large_delay_instance_all_rasters(dev, flags):
     # the drop-in (AUTO) path on the same instance
     got = api.dedisperse_tiled(fb, table, K(40, 1, 10, 4))
     assert np.array_equal(_bits(got.data), _bits(ref))
+
+
+@pytest.mark.parametrize("name,d", [("Apertif", 64), ("LOFAR", 32)])
+def test_every_gpu_space_config_is_bit_exact(dev, name, d):
+    """Every configuration the GPU tuner can select (dd_enumerate_gpu_configs:
+    all families, depths, stage shapes, rasters, occupancy builds) reproduces
+    the reference on one instance -- the auto-tuner may pick any of them."""
+    import torch
+    setup = api.find_builtin(name)
+    table = api.build_delay_table(setup, d)
+    t = api.instance_sizing(setup, d).num_samples
+    s, c = setup.samples_per_second, setup.channels
+    fb = api.noise_filterbank(setup, t, 1.0, 5)
+    rows = [0, d // 2, d - 1]
+    ref = O.dedisperse_reference(fb.data, table.shifts[rows], s)
+    x = torch.from_numpy(fb.data).cuda()
+    sh = torch.from_numpy(table.shifts.view(np.int32)).cuda()
+    out = torch.empty((d, s), device="cuda")
+    space = api.enumerate_gpu_configs(setup, d)
+    assert len(space) > 100
+    families = set()
+    for cfg, depth, staging, flags in space:
+        out.fill_(float("nan"))
+        p = dev.plan(sh.data_ptr(), c, d, s, t, t, cfg, depth, staging, flags=flags)
+        families.add(p.info()["family"])
+        p.execute(x.data_ptr(), out.data_ptr())
+        dev.synchronize()
+        got = out[rows].cpu().numpy()
+        assert np.array_equal(_bits(got), _bits(ref)), (cfg, depth, staging, hex(flags))
+        p.close()
+    assert {"smem", "direct"} <= families
