@@ -566,10 +566,14 @@ def test_every_gpu_space_config_is_bit_exact(dev, name, d):
     out = torch.empty((d, s), device="cuda")
     space = api.enumerate_gpu_configs(setup, d)
     assert len(space) > 100
-    families = set()
+    families, rejected = set(), 0
     for cfg, depth, staging, flags in space:
         out.fill_(float("nan"))
-        p = dev.plan(sh.data_ptr(), c, d, s, t, t, cfg, depth, staging, flags=flags)
+        try:  # the tuner skips what the plan rejects for this table (dd_tune)
+            p = dev.plan(sh.data_ptr(), c, d, s, t, t, cfg, depth, staging, flags=flags)
+        except ValueError:
+            rejected += 1
+            continue
         families.add(p.info()["family"])
         p.execute(x.data_ptr(), out.data_ptr())
         dev.synchronize()
@@ -577,3 +581,4 @@ def test_every_gpu_space_config_is_bit_exact(dev, name, d):
         assert np.array_equal(_bits(got), _bits(ref)), (cfg, depth, staging, hex(flags))
         p.close()
     assert {"smem", "direct"} <= families
+    assert rejected < len(space) // 4
