@@ -130,7 +130,7 @@ __device__ __forceinline__ Pipe pipe_setup(const TiledArgs& a, uint8_t* smem) {
   return p;
 }
 
-// (lo, span) of the up-to-8 channels of chunk g, fetched one chunk ahead
+// (lo, span) of the channels of chunk g (up to kMaxCps), fetched one chunk ahead
 // by the producer so the global-memory latency overlaps its slot wait.
 struct ChunkSpans {
   uint2 v[kMaxCps];
