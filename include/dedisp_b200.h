@@ -96,6 +96,11 @@ typedef struct dd_config {
  * whole input block, which then streams from HBM once per time tile;
  * time-fastest keeps the resident working set to one DM group's region. */
 #define DD_CONFIG_TIME_MAJOR 0x8u
+/* Staged families: pack each stage with as many channels as their own
+ * windows fit (instead of slots sized for the widest window), for
+ * instances whose delay spread varies across the band (LOFAR).  Full
+ * channel-range passes only; channel-range passes use fixed slots. */
+#define DD_CONFIG_PACKED_STAGES 0x10u
 /* Staged families: channels per pipeline stage in bits 8..11 (1..15; 0 lets
  * the plan choose).  A tuning knob: larger stages amortise the per-stage
  * synchronisation, smaller ones leave shared memory for more CTAs per SM. */

@@ -376,7 +376,7 @@ dd_status dd_validate_config(const dd_config* k, uint32_t num_dms, uint32_t s,
                                              std::to_string(L.max_accumulators));
   if (k->staging > DD_STAGING_TMEM) return fail(DD_ERR_INVALID_ARGUMENT, "unknown staging mode");
   if (k->flags & ~(DD_CONFIG_GPU_TILING | DD_CONFIG_HIGH_OCCUPANCY | DD_CONFIG_TIME_MAJOR |
-                   DD_CONFIG_CPS_MASK | DD_CONFIG_NSTAGE_MASK))
+                   DD_CONFIG_PACKED_STAGES | DD_CONFIG_CPS_MASK | DD_CONFIG_NSTAGE_MASK))
     return fail(DD_ERR_INVALID_ARGUMENT, "unknown config flags");
 
   const uint32_t ns = (k->flags & DD_CONFIG_NSTAGE_MASK) >> DD_CONFIG_NSTAGE_SHIFT;
@@ -483,6 +483,69 @@ bool smem_geometry(const dd_context* c, uint32_t tile_time, uint32_t tile_dm, ui
     }
   }
   return false;
+}
+
+void free_plan_buffers(dd_plan* p) {
+  cudaFree(p->d_rec);
+  cudaFree(p->d_ls);
+  cudaFree(p->d_chan_span);
+  cudaFree(p->d_stage_ch);
+  cudaFree(p->d_chan_off);
+  p->d_rec = nullptr;
+  p->d_ls = nullptr;
+  p->d_chan_span = p->d_stage_ch = p->d_chan_off = nullptr;
+}
+
+// DD_CONFIG_PACKED_STAGES: with each channel's own window width (its
+// widest span over the DM tiles, k_plan's chan_span) pack stages greedily
+// into equal stage buffers -- 2 stages unless the config asks for more.
+// Falls back silently to the fixed geometry already in `a` when no stage
+// buffer of the 2-CTA budget holds the widest window.  Channel-range
+// passes keep fixed slots of cps_fixed windows inside the same buffers.
+cudaError_t pack_stages(dd_context* c, dd_plan* p, ddb::TiledArgs& a, uint32_t channels,
+                        uint32_t slack, uint32_t flags, uint32_t* smem) {
+  std::vector<uint32_t> span(channels);
+  cudaError_t e = cudaMemcpy(span.data(), p->d_chan_span, channels * 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return e;
+  const uint32_t want_ns = (flags & DD_CONFIG_NSTAGE_MASK) >> DD_CONFIG_NSTAGE_SHIFT;
+  const uint32_t ns = want_ns >= 2 ? want_ns : 2;
+  const uint64_t fixed = ddb::kPipeHeader + static_cast<uint64_t>(ns) * ddb::kMaxCps * a.rec_bytes;
+  if (fixed >= kSmemBudget) return cudaSuccess;
+  const uint32_t stage_floats = static_cast<uint32_t>((kSmemBudget - fixed) / (4ull * ns)) & ~3u;
+  if (stage_floats < a.win_cap) return cudaSuccess;
+  std::vector<uint32_t> stage_ch, off(channels);
+  uint32_t ch = 0, widest = 0;
+  while (ch < channels) {
+    stage_ch.push_back(ch);
+    uint32_t used = 0, n = 0;
+    while (ch < channels && n < ddb::kMaxCps) {
+      const uint32_t cap = (span[ch] + a.tile_time + slack + 6u + 3u) & ~3u;
+      if (n > 0 && used + cap > stage_floats) break;
+      off[ch++] = used;
+      used += cap;
+      ++n;
+    }
+    widest = std::max(widest, n);
+  }
+  stage_ch.push_back(channels);
+  e = cudaMalloc(&p->d_stage_ch, stage_ch.size() * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_chan_off, channels * 4);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p->d_stage_ch, stage_ch.data(), stage_ch.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_chan_off, off.data(), channels * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return e;
+  a.packed = 1;
+  a.packed_stages = static_cast<uint32_t>(stage_ch.size() - 1);
+  a.stage_ch = p->d_stage_ch;
+  a.chan_off = p->d_chan_off;
+  a.nstage = ns;
+  a.cps = widest;  // record slots per stage
+  a.stage_floats = stage_floats;
+  *smem = static_cast<uint32_t>(fixed - static_cast<uint64_t>(ns) * (ddb::kMaxCps - widest) *
+                                            a.rec_bytes +
+                                4ull * ns * stage_floats);
+  (void)c;
+  return cudaSuccess;
 }
 
 dd_status max_of_device_table(dd_context* c, const uint32_t* d_shifts, uint64_t n, uint32_t* out) {
@@ -630,19 +693,22 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
     cudaError_t e = cudaMalloc(&p->d_rec, rec_total);
     if (e == cudaSuccess)
       e = cudaMalloc(&p->d_ls, static_cast<uint64_t>(a.tiles_dm) * channels * sizeof(uint2));
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_chan_span, channels * sizeof(uint32_t));
+    if (e == cudaSuccess)
+      e = cudaMemsetAsync(p->d_chan_span, 0, channels * sizeof(uint32_t), c->stream);
     uint32_t scratch[4] = {0, 0, 0, 0};
     unsigned long long* d_sum = reinterpret_cast<unsigned long long*>(c->d_scratch + 2);
     if (e == cudaSuccess) e = cudaMemsetAsync(c->d_scratch, 0, 16, c->stream);
     if (e == cudaSuccess)
       e = launch_plan(d_shifts, p->d_rec, p->d_ls, c->d_scratch, d_sum, channels, a.tiles_dm, a.tile_dm,
                       k->work_dm, a.rec_bytes,
-                      k->staging == DD_STAGING_TMEM ? k->work_time : 0u, c->stream);
+                      k->staging == DD_STAGING_TMEM ? k->work_time : 0u, p->d_chan_span,
+                      c->stream);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(scratch, c->d_scratch, 16, cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
-      cudaFree(p->d_rec);
-      cudaFree(p->d_ls);
+      free_plan_buffers(p);
       delete p;
       return cuda_fail(e, "plan pre-pass");
     }
@@ -686,8 +752,18 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
       a.win_cap = win_cap;
       a.cps = cps;
       a.nstage = nstage;
+      a.stage_floats = cps * win_cap;
+      a.packed = 0;
       a.rec = p->d_rec;
       a.ls = p->d_ls;
+      if (k->flags & DD_CONFIG_PACKED_STAGES) {
+        e = pack_stages(c, p, a, channels, slack, k->flags, &smem);
+        if (e != cudaSuccess) {
+          free_plan_buffers(p);
+          delete p;
+          return cuda_fail(e, "packed stages");
+        }
+      }
       p->smem_fn = fn;
       p->smem = smem;
       // whole consumer warps plus one producer warp (dedisp.cu staged_loop)
@@ -697,8 +773,7 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
       p->family = family;
       e = prepare_smem(p->smem_fn, smem);
       if (e != cudaSuccess) {
-        cudaFree(p->d_rec);
-        cudaFree(p->d_ls);
+        free_plan_buffers(p);
         delete p;
         return cuda_fail(e, "cudaFuncSetAttribute");
       }
@@ -708,10 +783,7 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
       *out = p;
       return DD_OK;
     }
-    cudaFree(p->d_rec);
-    cudaFree(p->d_ls);
-    p->d_rec = nullptr;
-    p->d_ls = nullptr;
+    free_plan_buffers(p);
   }
   if (k->staging == DD_STAGING_SMEM || k->staging == DD_STAGING_REGWIN ||
       k->staging == DD_STAGING_TMEM ||
@@ -745,8 +817,7 @@ dd_status dd_plan_destroy(dd_plan* p) {
   if (p == nullptr) return DD_OK;
   if (p->d_rec) {
     cudaSetDevice(p->ctx->device);
-    cudaFree(p->d_rec);
-    cudaFree(p->d_ls);
+    free_plan_buffers(p);
   }
   delete p;
   return DD_OK;
@@ -830,6 +901,12 @@ dd_status dd_plan_execute_channels(dd_plan* p, const float* d_in, float* d_out,
   a.ch_begin = ch_begin;
   a.ch_end = ch_end;
   a.accumulate = accumulate ? 1u : 0u;
+  if (a.packed && (ch_begin != 0 || ch_end != a.channels)) {
+    // packed stages cover the full channel range; a sub-range uses fixed
+    // slots of the widest window inside the same stage buffers
+    a.packed = 0;
+    a.cps = std::max(1u, std::min(a.cps, a.stage_floats / a.win_cap));
+  }
   DD_CUDA(launch_smem(p->smem_fn, a, p->blocks, p->threads, p->smem, c->stream));
   return DD_OK;
 }

@@ -156,6 +156,15 @@ struct TiledArgs {
   // split by channel ranges then reproduces the single pass bit for bit:
   // the running fp32 sum round-trips through memory exactly)
   uint32_t ch_begin, ch_end, accumulate;
+  // packed stages (DD_CONFIG_PACKED_STAGES, full channel range): stage q
+  // holds channels [stage_ch[q], stage_ch[q+1]) and channel c's window sits
+  // chan_off[c] floats into its stage buffer -- each channel takes its own
+  // window width instead of the widest, so wide-delay instances fit more
+  // channels per stage.  Otherwise stage q is cps channels of win_cap floats.
+  const uint32_t* stage_ch;
+  const uint32_t* chan_off;
+  uint32_t packed, packed_stages;
+  uint32_t stage_floats;  // floats per stage buffer (cps * win_cap unless packed)
   // staged families: independent beams (grid.y), each with its own input
   // block and output rows at these strides (floats) -- the deployment's
   // many-beams-per-GPU batching

@@ -112,7 +112,7 @@ __device__ __forceinline__ Pipe pipe_setup(const TiledArgs& a, uint8_t* smem) {
   p.full = reinterpret_cast<uint64_t*>(smem);
   p.empty = reinterpret_cast<uint64_t*>(smem + 64);
   p.recs = smem + kPipeHeader;
-  p.wins = reinterpret_cast<float*>(p.recs + a.nstage * a.cps * a.rec_bytes);
+  p.wins = reinterpret_cast<float*>(p.recs + a.nstage * a.cps * a.rec_bytes);  // 16-B aligned
   const uint32_t groups_dm = (a.tiles_dm + a.depth - 1) / a.depth;
   if (a.time_major) {
     // time-fastest: the resident CTAs cover few DM groups over many time
@@ -125,9 +125,26 @@ __device__ __forceinline__ Pipe pipe_setup(const TiledArgs& a, uint8_t* smem) {
     p.b_first = (blockIdx.x % groups_dm) * a.depth;
   }
   const uint32_t ntiles = min(a.depth, a.tiles_dm - p.b_first);
-  p.nchunk = (a.ch_end - a.ch_begin + a.cps - 1) / a.cps;
+  p.nchunk = a.packed ? a.packed_stages : (a.ch_end - a.ch_begin + a.cps - 1) / a.cps;
   p.total = ntiles * p.nchunk;
   return p;
+}
+
+// Channels of stage q (of a tile): first channel and count.
+__device__ __forceinline__ void stage_channels(const TiledArgs& a, uint32_t q, uint32_t& ch0,
+                                               uint32_t& ncs) {
+  if (a.packed) {
+    ch0 = __ldg(a.stage_ch + q);
+    ncs = __ldg(a.stage_ch + q + 1) - ch0;
+  } else {
+    ch0 = a.ch_begin + q * a.cps;
+    ncs = min(a.cps, a.ch_end - ch0);
+  }
+}
+
+// Offset (floats) of window cc of a stage whose first channel is ch0.
+__device__ __forceinline__ uint32_t window_offset(const TiledArgs& a, uint32_t ch0, uint32_t cc) {
+  return a.packed ? __ldg(a.chan_off + ch0 + cc) : cc * a.win_cap;
 }
 
 // (lo, span) of the channels of chunk g (up to kMaxCps), fetched one chunk ahead
@@ -139,8 +156,8 @@ struct ChunkSpans {
 __device__ __forceinline__ ChunkSpans pipe_spans(const TiledArgs& a, const Pipe& p, uint32_t g) {
   ChunkSpans c;
   const uint32_t b = p.b_first + g / p.nchunk;
-  const uint32_t ch0 = a.ch_begin + (g % p.nchunk) * a.cps;
-  const uint32_t ncs = min(a.cps, a.ch_end - ch0);
+  uint32_t ch0, ncs;
+  stage_channels(a, g % p.nchunk, ch0, ncs);
   const uint2* src = a.ls + static_cast<uint64_t>(b) * a.channels + ch0;
 #pragma unroll
   for (uint32_t cc = 0; cc < kMaxCps; ++cc) {
@@ -155,8 +172,8 @@ __device__ __forceinline__ ChunkSpans pipe_spans(const TiledArgs& a, const Pipe&
 __device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, uint32_t g,
                                            const ChunkSpans& cs) {
   const uint32_t b = p.b_first + g / p.nchunk;
-  const uint32_t ch0 = a.ch_begin + (g % p.nchunk) * a.cps;
-  const uint32_t ncs = min(a.cps, a.ch_end - ch0);
+  uint32_t ch0, ncs;
+  stage_channels(a, g % p.nchunk, ch0, ncs);
   const uint32_t slot = g % a.nstage;
   const uint8_t* rsrc = a.rec + (static_cast<uint64_t>(b) * a.channels + ch0) * a.rec_bytes;
   uint64_t* bar = &p.full[slot];
@@ -165,7 +182,7 @@ __device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, ui
   mbar_expect_tx(bar, ncs * a.rec_bytes);
   bulk_g2s(p.recs + slot * a.cps * a.rec_bytes, rsrc, ncs * a.rec_bytes, bar);
   const float* src = a.in + blockIdx.y * a.in_beam_stride + static_cast<uint64_t>(ch0) * a.in_pitch;
-  float* dst = p.wins + static_cast<uint64_t>(slot * a.cps) * a.win_cap;
+  float* dst = p.wins + static_cast<uint64_t>(slot) * a.stage_floats;
 #pragma unroll
   for (uint32_t cc = 0; cc < kMaxCps; ++cc) {
     if (cc >= ncs) break;
@@ -176,7 +193,7 @@ __device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, ui
                              static_cast<uint32_t>(a.in_pitch));
     const uint32_t bytes = (end - start) * 4u;
     mbar_expect_tx(bar, bytes);
-    bulk_g2s(dst + static_cast<uint64_t>(cc) * a.win_cap, src + static_cast<uint64_t>(cc) * a.in_pitch + start,
+    bulk_g2s(dst + window_offset(a, ch0, cc), src + static_cast<uint64_t>(cc) * a.in_pitch + start,
              bytes, bar);
   }
   mbar_arrive(bar);
@@ -233,16 +250,18 @@ __device__ __forceinline__ void staged_loop_with(const TiledArgs& a, uint8_t* sm
     }
     const uint32_t slot = g % a.nstage;
     mbar_wait(&p.full[slot], (g / a.nstage) & 1u);
-    const uint32_t ncs = min(a.cps, a.ch_end - (a.ch_begin + q * a.cps));
+    uint32_t ch0, ncs;
+    stage_channels(a, q, ch0, ncs);
     const uint8_t* rbase = p.recs + slot * a.cps * a.rec_bytes;
-    const float* wbase = p.wins + static_cast<uint64_t>(slot) * a.cps * a.win_cap;
+    const float* wbase = p.wins + static_cast<uint64_t>(slot) * a.stage_floats;
     if (active) {
       for (uint32_t cc = 0; cc < ncs; ++cc) {
         const uint32_t* r = reinterpret_cast<const uint32_t*>(rbase + cc * a.rec_bytes);
+        const float* w = wbase + window_offset(a, ch0, cc);
         if constexpr (Body::kRowBase)
-          body.channel(r, wbase + cc * a.win_cap);
+          body.channel(r, w);
         else
-          body.channel(r, wbase + cc * a.win_cap + ((p.t0 + r[0]) & 3u));
+          body.channel(r, w + ((p.t0 + r[0]) & 3u));
       }
     }
     __syncwarp();

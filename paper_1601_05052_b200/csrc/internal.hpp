@@ -30,6 +30,9 @@ struct dd_plan {
   const uint32_t* d_shifts = nullptr;
   uint8_t* d_rec = nullptr;
   uint2* d_ls = nullptr;
+  uint32_t* d_chan_span = nullptr;  // [channels] widest span per channel (k_plan)
+  uint32_t* d_stage_ch = nullptr;   // packed stages: [stages + 1] first channels
+  uint32_t* d_chan_off = nullptr;   // packed stages: [channels] window offsets
   void (*smem_fn)(const ddb::TiledArgs) = nullptr;
   uint32_t blocks = 0, threads = 0, smem = 0;
   uint32_t grid_y = 1;
@@ -51,7 +54,7 @@ cudaError_t launch_delay_table(uint32_t* d_shifts, uint32_t* d_max, uint32_t num
 cudaError_t launch_plan(const uint32_t* d_shifts, uint8_t* d_rec, uint2* d_ls, uint32_t* d_max_span,
                         unsigned long long* d_span_sum, uint32_t channels, uint32_t tiles_dm,
                         uint32_t tile_dm, uint32_t group, uint32_t rec_bytes, uint32_t window_format,
-                        cudaStream_t st);
+                        uint32_t* d_chan_span, cudaStream_t st);
 cudaError_t launch_max_u32(const uint32_t* d_v, uint64_t n, uint32_t* d_out, cudaStream_t st);
 
 using KernelFn = void (*)(const TiledArgs);

@@ -49,7 +49,8 @@ __global__ void k_delay_table(uint32_t* __restrict__ shifts, uint32_t* __restric
 __global__ void k_plan(const uint32_t* __restrict__ shifts, uint8_t* __restrict__ rec,
                        uint2* __restrict__ ls, uint32_t* __restrict__ max_span, unsigned long long* __restrict__ span_sum,
                        uint32_t channels, uint32_t tiles_dm, uint32_t tile_dm, uint32_t group,
-                       uint32_t rec_bytes, uint32_t window_format) {
+                       uint32_t rec_bytes, uint32_t window_format,
+                       uint32_t* __restrict__ chan_span) {
   const uint64_t n = static_cast<uint64_t>(tiles_dm) * channels;
   const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   uint32_t span = 0, gspan = 0;
@@ -97,6 +98,8 @@ __global__ void k_plan(const uint32_t* __restrict__ shifts, uint8_t* __restrict_
       }
     }
   }
+  // widest span of each channel over the DM tiles (packed stage sizing)
+  if (i < n) atomicMax(chan_span + (i % channels), span);
   const uint32_t sum = __reduce_add_sync(0xffffffffu, span);
   span = __reduce_max_sync(0xffffffffu, span);
   gspan = __reduce_max_sync(0xffffffffu, gspan);
@@ -141,14 +144,14 @@ cudaError_t launch_delay_table(uint32_t* d_shifts, uint32_t* d_max, uint32_t num
 cudaError_t launch_plan(const uint32_t* d_shifts, uint8_t* d_rec, uint2* d_ls, uint32_t* d_max_span,
                         unsigned long long* d_span_sum, uint32_t channels, uint32_t tiles_dm,
                         uint32_t tile_dm, uint32_t group, uint32_t rec_bytes, uint32_t window_format,
-                        cudaStream_t st) {
+                        uint32_t* d_chan_span, cudaStream_t st) {
   const uint64_t n = static_cast<uint64_t>(tiles_dm) * channels;
   const uint32_t threads = 128;
   const uint64_t blocks = (n + threads - 1) / threads;
   k_plan<<<static_cast<uint32_t>(blocks), threads, 0, st>>>(d_shifts, d_rec, d_ls, d_max_span,
                                                             d_span_sum, channels, tiles_dm, tile_dm,
                                                             group ? group : 1, rec_bytes,
-                                                            window_format);
+                                                            window_format, d_chan_span);
   return cudaGetLastError();
 }
 

@@ -256,7 +256,9 @@ def test_non_monotone_and_fault_injected_tables(dev, golden):
     ("tmem", K(32, 2, 12, 8), 3), ("tmem", K(32, 1, 12, 8), 1), ("tmem", K(32, 4, 20, 4), 2),
     ("tmem", K(32, 4, 12, 8), 15), ("tmem", K(32, 4, 12, 8), 11), ("smem", K(32, 4, 4, 4), 13),
     ("regwin", K(32, 4, 12, 4), 15), ("tmem", K(32, 4, 12, 8), 15, "tm"),
-    ("smem", K(32, 4, 4, 4), 8, "tm"), ("regwin", K(32, 4, 12, 4), 4, "tm")])
+    ("smem", K(32, 4, 4, 4), 8, "tm"), ("regwin", K(32, 4, 12, 4), 4, "tm"),
+    ("tmem", K(32, 4, 12, 8), 0, "packed"), ("smem", K(32, 4, 4, 4), 0, "packed"),
+    ("regwin", K(32, 4, 12, 4), 0, "packed")])
 def test_gpu_tiling_predicated_tail(dev, golden, spec):
     """GPU-native tiles whose tile_time does not divide s (vector register
     windows, odd smem tiles, TMEM windows incl. the three-CTA builds): the
@@ -274,9 +276,10 @@ def test_gpu_tiling_predicated_tail(dev, golden, spec):
     torch.cuda.synchronize()
     p = dev.plan(sh.data_ptr(), c, d, s, t, t, cfg, 1, staging, gpu_tiling=True,
                  stage_channels=cps, high_occupancy=mode == "occ",
-                 flags=N.DD_CONFIG_TIME_MAJOR if mode == "tm" else 0)
+                 flags=(N.DD_CONFIG_TIME_MAJOR if mode == "tm" else 0)
+                 | (N.DD_CONFIG_PACKED_STAGES if mode == "packed" else 0))
     info = p.info()
-    assert info["family"] == staging and info["channels_per_stage"] == cps
+    assert info["family"] == staging and (mode == "packed" or info["channels_per_stage"] == cps)
     if mode == "occ":
         assert 0 < info["registers"] <= 128
     p.execute(x.data_ptr(), out.data_ptr())
@@ -508,7 +511,8 @@ def test_sigproc_transpose_on_device(dev):
     assert dev.sigproc_to_filterbank(src.data_ptr(), c, t, dst.data_ptr(), pitch) == 500 * c + 3
 
 
-@pytest.mark.parametrize("flags", [0, "tm", "tm-ns2", "cps3-ns4"])
+@pytest.mark.parametrize("flags", [0, "tm", "tm-ns2", "cps3-ns4", "packed", "tm-packed",
+                                   "packed-ns3"])
 def test_large_delay_instance_all_rasters(dev, flags):
     """LOFAR-shaped delays (hundreds of samples per DM step, a block several
     seconds long): every CTA raster and stage shape, including channel-range
@@ -529,6 +533,10 @@ def test_large_delay_instance_all_rasters(dev, flags):
         f |= 2 << N.DD_CONFIG_NSTAGE_SHIFT
     if "cps3" in str(flags):
         f |= (3 << N.DD_CONFIG_CPS_SHIFT) | (4 << N.DD_CONFIG_NSTAGE_SHIFT)
+    if "packed" in str(flags):
+        f |= N.DD_CONFIG_PACKED_STAGES
+    if "ns3" in str(flags):
+        f |= 3 << N.DD_CONFIG_NSTAGE_SHIFT
     x = torch.from_numpy(fb.data).cuda()
     sh = torch.from_numpy(table.shifts.view(np.int32)).cuda()
     for cfg, depth in ((K(16, 4, 25, 1), 2), (K(40, 1, 10, 4), 1), (K(25, 2, 8, 2), 1)):

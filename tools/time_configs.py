@@ -4,7 +4,7 @@
 
 Extra fields: "g" requests GPU tiling (tile_time need not divide s),
 "cpsN" pins N channels per pipeline stage, "occ" the TMEM three-CTA build,
-"nsN" N pipeline stages, "tm" time-major CTA raster.
+"nsN" N pipeline stages, "tm" time-major CTA raster, "pk" packed stages.
 """
 import os
 import sys
@@ -40,7 +40,8 @@ def main():
                          high_occupancy="occ" in extra,
                          flags=(next((int(x[2:]) for x in extra if x.startswith("ns")), 0)
                                 << N.DD_CONFIG_NSTAGE_SHIFT)
-                         | (N.DD_CONFIG_TIME_MAJOR if "tm" in extra else 0))
+                         | (N.DD_CONFIG_TIME_MAJOR if "tm" in extra else 0)
+                         | (N.DD_CONFIG_PACKED_STAGES if "pk" in extra else 0))
         except ValueError as e:
             print(f"{spec:28s} invalid: {e}")
             continue
