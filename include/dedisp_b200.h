@@ -220,6 +220,7 @@ typedef struct dd_plan_info {
                            * staged); conservative for the tcgen05 (TMEM) kernels,
                            * which it reports as 1 while two run (ncu: ~10 warps/SM) */
   uint32_t time_major;    /* CTA raster time-fastest (DD_CONFIG_TIME_MAJOR or AUTO's pick) */
+  uint32_t packed_stages; /* stages per tile when packed (DD_CONFIG_PACKED_STAGES), else 0 */
 } dd_plan_info;
 dd_status dd_plan_get_info(const dd_plan* plan, dd_plan_info* info);
 

@@ -63,7 +63,8 @@ class dd_plan_info(C.Structure):
                 ("smem_bytes", C.c_uint32), ("channels_per_stage", C.c_uint32),
                 ("stages", C.c_uint32), ("kernel_launches", C.c_uint32),
                 ("staged_bytes", C.c_uint64), ("registers", C.c_uint32),
-                ("ctas_per_sm", C.c_uint32), ("time_major", C.c_uint32)]
+                ("ctas_per_sm", C.c_uint32), ("time_major", C.c_uint32),
+                ("packed_stages", C.c_uint32)]
 
 
 class dd_tune_options(C.Structure):

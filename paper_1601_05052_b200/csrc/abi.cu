@@ -722,7 +722,7 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
       // AUTO: the shared-memory kernel (fastest measured family, round 1),
     // register windows where it has no variant.
     family = smem_shape ? DD_STAGING_SMEM : DD_STAGING_REGWIN;
-    ddb::KernelFn fn = nullptr;
+    ddb::KernelFn fn = nullptr, fn_packed = nullptr;
     uint32_t slack = 0;
     if (family == DD_STAGING_REGWIN) {
       fn = find_regwin_kernel(k->work_dm, k->work_time, p->group_span, &p->regwin_span);
@@ -736,7 +736,7 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
         fn = find_tmem_kernel(k->work_dm, k->work_time, p->group_span, &p->regwin_span);
       slack = p->regwin_span + 8;
     } else {
-      fn = find_smem_kernel(k->work_dm, k->work_time, nullptr, k->items_time);
+      fn = find_smem_kernel(k->work_dm, k->work_time, nullptr, k->items_time, &fn_packed);
     }
     uint32_t win_cap = 0, rec_bytes = 0, cps = 0, nstage = 0, smem = 0;
     // the launch must fit the variant's register budget
@@ -756,13 +756,16 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
       a.packed = 0;
       a.rec = p->d_rec;
       a.ls = p->d_ls;
-      if (k->flags & DD_CONFIG_PACKED_STAGES) {
+      p->smem_fn_fixed = fn;
+      if ((k->flags & DD_CONFIG_PACKED_STAGES) && fn_packed != nullptr) {
+        // only the K3 shapes with a packed build; otherwise the flag is a no-op
         e = pack_stages(c, p, a, channels, slack, k->flags, &smem);
         if (e != cudaSuccess) {
           free_plan_buffers(p);
           delete p;
           return cuda_fail(e, "packed stages");
         }
+        if (a.packed) fn = fn_packed;
       }
       p->smem_fn = fn;
       p->smem = smem;
@@ -772,6 +775,7 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
       p->blocks = static_cast<uint32_t>(groups_dm * a.tiles_time);
       p->family = family;
       e = prepare_smem(p->smem_fn, smem);
+      if (e == cudaSuccess && p->smem_fn_fixed != p->smem_fn) e = prepare_smem(p->smem_fn_fixed, smem);
       if (e != cudaSuccess) {
         free_plan_buffers(p);
         delete p;
@@ -838,6 +842,7 @@ dd_status dd_plan_get_info(const dd_plan* p, dd_plan_info* info) {
   info->kernel_launches = 1;
   info->staged_bytes = p->staged_bytes;
   info->time_major = p->args.time_major;
+  info->packed_stages = p->args.packed ? p->args.packed_stages : 0;
   if (p->smem_fn != nullptr) {
     cudaFuncAttributes fa{};
     int ctas = 0;
@@ -901,13 +906,17 @@ dd_status dd_plan_execute_channels(dd_plan* p, const float* d_in, float* d_out,
   a.ch_begin = ch_begin;
   a.ch_end = ch_end;
   a.accumulate = accumulate ? 1u : 0u;
+  ddb::KernelFn fn = p->smem_fn;
   if (a.packed && (ch_begin != 0 || ch_end != a.channels)) {
-    // packed stages cover the full channel range; a sub-range uses fixed
-    // slots of the widest window inside the same stage buffers
+    // packed stages cover the full channel range; a sub-range runs the fixed
+    // build with slots of the widest window inside the same stage buffers
     a.packed = 0;
     a.cps = std::max(1u, std::min(a.cps, a.stage_floats / a.win_cap));
+    a.win_cap = a.stage_floats / a.cps;  // (fixed build strides slot * cps * win_cap)
+    a.win_cap &= ~3u;
+    fn = p->smem_fn_fixed;
   }
-  DD_CUDA(launch_smem(p->smem_fn, a, p->blocks, p->threads, p->smem, c->stream));
+  DD_CUDA(launch_smem(fn, a, p->blocks, p->threads, p->smem, c->stream));
   return DD_OK;
 }
 

@@ -107,6 +107,7 @@ struct Pipe {
   uint32_t t0, b_first, nchunk, total;
 };
 
+template <bool PK>
 __device__ __forceinline__ Pipe pipe_setup(const TiledArgs& a, uint8_t* smem) {
   Pipe p;
   p.full = reinterpret_cast<uint64_t*>(smem);
@@ -125,15 +126,21 @@ __device__ __forceinline__ Pipe pipe_setup(const TiledArgs& a, uint8_t* smem) {
     p.b_first = (blockIdx.x % groups_dm) * a.depth;
   }
   const uint32_t ntiles = min(a.depth, a.tiles_dm - p.b_first);
-  p.nchunk = a.packed ? a.packed_stages : (a.ch_end - a.ch_begin + a.cps - 1) / a.cps;
+  if constexpr (PK)
+    p.nchunk = a.packed_stages;
+  else
+    p.nchunk = (a.ch_end - a.ch_begin + a.cps - 1) / a.cps;
   p.total = ntiles * p.nchunk;
   return p;
 }
 
-// Channels of stage q (of a tile): first channel and count.
+// Channels of stage q (of a tile): first channel and count.  PK (packed
+// stages, compile time: a runtime switch here cost every build ~15%) reads
+// the plan's stage table.
+template <bool PK>
 __device__ __forceinline__ void stage_channels(const TiledArgs& a, uint32_t q, uint32_t& ch0,
                                                uint32_t& ncs) {
-  if (a.packed) {
+  if constexpr (PK) {
     ch0 = __ldg(a.stage_ch + q);
     ncs = __ldg(a.stage_ch + q + 1) - ch0;
   } else {
@@ -142,9 +149,21 @@ __device__ __forceinline__ void stage_channels(const TiledArgs& a, uint32_t q, u
   }
 }
 
-// Offset (floats) of window cc of a stage whose first channel is ch0.
+// Offset (floats) of window cc of a stage whose first channel is ch0, and
+// of a stage buffer.
+template <bool PK>
 __device__ __forceinline__ uint32_t window_offset(const TiledArgs& a, uint32_t ch0, uint32_t cc) {
-  return a.packed ? __ldg(a.chan_off + ch0 + cc) : cc * a.win_cap;
+  if constexpr (PK)
+    return __ldg(a.chan_off + ch0 + cc);
+  else
+    return cc * a.win_cap;
+}
+template <bool PK>
+__device__ __forceinline__ uint64_t stage_offset(const TiledArgs& a, uint32_t slot) {
+  if constexpr (PK)
+    return static_cast<uint64_t>(slot) * a.stage_floats;
+  else
+    return static_cast<uint64_t>(slot * a.cps) * a.win_cap;
 }
 
 // (lo, span) of the channels of chunk g (up to kMaxCps), fetched one chunk ahead
@@ -153,11 +172,12 @@ struct ChunkSpans {
   uint2 v[kMaxCps];
 };
 
+template <bool PK>
 __device__ __forceinline__ ChunkSpans pipe_spans(const TiledArgs& a, const Pipe& p, uint32_t g) {
   ChunkSpans c;
   const uint32_t b = p.b_first + g / p.nchunk;
   uint32_t ch0, ncs;
-  stage_channels(a, g % p.nchunk, ch0, ncs);
+  stage_channels<PK>(a, g % p.nchunk, ch0, ncs);
   const uint2* src = a.ls + static_cast<uint64_t>(b) * a.channels + ch0;
 #pragma unroll
   for (uint32_t cc = 0; cc < kMaxCps; ++cc) {
@@ -169,11 +189,12 @@ __device__ __forceinline__ ChunkSpans pipe_spans(const TiledArgs& a, const Pipe&
 
 // Stage chunk g = (tile, channel group) into its slot: one bulk copy for the
 // chunk's plan records, one per channel window, all counted on full[slot].
+template <bool PK>
 __device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, uint32_t g,
                                            const ChunkSpans& cs) {
   const uint32_t b = p.b_first + g / p.nchunk;
   uint32_t ch0, ncs;
-  stage_channels(a, g % p.nchunk, ch0, ncs);
+  stage_channels<PK>(a, g % p.nchunk, ch0, ncs);
   const uint32_t slot = g % a.nstage;
   const uint8_t* rsrc = a.rec + (static_cast<uint64_t>(b) * a.channels + ch0) * a.rec_bytes;
   uint64_t* bar = &p.full[slot];
@@ -182,7 +203,7 @@ __device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, ui
   mbar_expect_tx(bar, ncs * a.rec_bytes);
   bulk_g2s(p.recs + slot * a.cps * a.rec_bytes, rsrc, ncs * a.rec_bytes, bar);
   const float* src = a.in + blockIdx.y * a.in_beam_stride + static_cast<uint64_t>(ch0) * a.in_pitch;
-  float* dst = p.wins + static_cast<uint64_t>(slot) * a.stage_floats;
+  float* dst = p.wins + stage_offset<PK>(a, slot);
 #pragma unroll
   for (uint32_t cc = 0; cc < kMaxCps; ++cc) {
     if (cc >= ncs) break;
@@ -193,21 +214,22 @@ __device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, ui
                              static_cast<uint32_t>(a.in_pitch));
     const uint32_t bytes = (end - start) * 4u;
     mbar_expect_tx(bar, bytes);
-    bulk_g2s(dst + window_offset(a, ch0, cc), src + static_cast<uint64_t>(cc) * a.in_pitch + start,
+    bulk_g2s(dst + window_offset<PK>(a, ch0, cc), src + static_cast<uint64_t>(cc) * a.in_pitch + start,
              bytes, bar);
   }
   mbar_arrive(bar);
 }
 
 // The producer lane: issue every chunk as soon as its slot is handed back.
+template <bool PK>
 __device__ __forceinline__ void pipe_produce(const TiledArgs& a, const Pipe& p) {
-  ChunkSpans next = pipe_spans(a, p, 0);
+  ChunkSpans next = pipe_spans<PK>(a, p, 0);
   for (uint32_t g = 0; g < p.total; ++g) {
     const ChunkSpans cur = next;
-    if (g + 1 < p.total) next = pipe_spans(a, p, g + 1);
+    if (g + 1 < p.total) next = pipe_spans<PK>(a, p, g + 1);
     const uint32_t use = g / a.nstage;
     if (use > 0) mbar_wait_sleep(&p.empty[g % a.nstage], (use - 1) & 1u);
-    pipe_issue(a, p, g, cur);
+    pipe_issue<PK>(a, p, g, cur);
   }
 }
 
@@ -221,7 +243,8 @@ __device__ __forceinline__ void pipe_produce(const TiledArgs& a, const Pipe& p) 
 template <class Body, class... Extra>
 __device__ __forceinline__ void staged_loop_with(const TiledArgs& a, uint8_t* smem,
                                                  Extra... extra) {
-  const Pipe p = pipe_setup(a, smem);
+  constexpr bool PK = Body::kPacked;
+  const Pipe p = pipe_setup<PK>(a, smem);
   const uint32_t tid = threadIdx.x;
   const uint32_t consumers = blockDim.x / 32 - 1;
   if (tid == 0) {
@@ -233,7 +256,7 @@ __device__ __forceinline__ void staged_loop_with(const TiledArgs& a, uint8_t* sm
   }
   __syncthreads();
   if (tid >= consumers * 32) {  // producer warp
-    if (tid == consumers * 32) pipe_produce(a, p);
+    if (tid == consumers * 32) pipe_produce<PK>(a, p);
     return;
   }
   // Consumer threads beyond the config's items (the block is rounded up to
@@ -251,13 +274,13 @@ __device__ __forceinline__ void staged_loop_with(const TiledArgs& a, uint8_t* sm
     const uint32_t slot = g % a.nstage;
     mbar_wait(&p.full[slot], (g / a.nstage) & 1u);
     uint32_t ch0, ncs;
-    stage_channels(a, q, ch0, ncs);
+    stage_channels<PK>(a, q, ch0, ncs);
     const uint8_t* rbase = p.recs + slot * a.cps * a.rec_bytes;
-    const float* wbase = p.wins + static_cast<uint64_t>(slot) * a.stage_floats;
+    const float* wbase = p.wins + stage_offset<PK>(a, slot);
     if (active) {
       for (uint32_t cc = 0; cc < ncs; ++cc) {
         const uint32_t* r = reinterpret_cast<const uint32_t*>(rbase + cc * a.rec_bytes);
-        const float* w = wbase + window_offset(a, ch0, cc);
+        const float* w = wbase + window_offset<PK>(a, ch0, cc);
         if constexpr (Body::kRowBase)
           body.channel(r, w);
         else
@@ -283,9 +306,10 @@ __device__ __forceinline__ void staged_loop(const TiledArgs& a, uint8_t* smem) {
 // conflict-free shared-memory wavefront per warp-load, one load per add.
 // Bound: shared-memory operand bandwidth (32 adds/clk/SM).
 // ---------------------------------------------------------------------
-template <int K, int W, int IT = 0>
+template <int K, int W, int IT = 0, bool PK = false>
 struct SmemBody {
   static constexpr bool kRowBase = false;  // channel() gets the row at lo's sample
+  static constexpr bool kPacked = PK;      // packed stages (compile time)
   const TiledArgs& a;
   uint32_t it, id;
   float acc[K][W];
@@ -341,10 +365,10 @@ constexpr int smem_max_threads() {
   return K * W > 32 ? 256 : (K * W > 16 ? 512 : 992);
 }
 
-template <int K, int W, int IT = 0>
+template <int K, int W, int IT = 0, bool PK = false>
 __global__ void __launch_bounds__(smem_max_threads<K, W>() + 32) k_smem(const TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  staged_loop<SmemBody<K, W, IT>>(a, smem);
+  staged_loop<SmemBody<K, W, IT, PK>>(a, smem);
 }
 
 // ---------------------------------------------------------------------
@@ -475,6 +499,7 @@ struct RegWin {
 template <int K, int W, int SPAN>
 struct RegWinBody {
   static constexpr bool kRowBase = false;
+  static constexpr bool kPacked = false;
   const TiledArgs& a;
   uint32_t col;  // first sample of this lane relative to t0
   uint32_t dml;  // first DM of this warp relative to dm0
@@ -593,6 +618,7 @@ __device__ __forceinline__ void tmem_wait_ld() {
 template <int K, int W, int SPAN, int COLS, bool FULL_HEAD = true>
 struct TmemBody {
   static constexpr bool kRowBase = true;  // channel() gets the 16-byte aligned row start
+  static constexpr bool kPacked = false;
   static_assert(W % 4 == 0, "16-byte window loads (W/4 odd is conflict-free, even is 2-way)");
   static_assert(COLS == 32 || COLS == 64, "32 or 64 TMEM columns per warp window");
   static_assert(W + SPAN + 3 <= COLS, "window must fit the warp's TMEM columns");
@@ -833,10 +859,13 @@ struct SmemVariant {
   int k, w, it;  // it = 0: items_time at run time
   KernelFn fn;
   int max_threads;
+  KernelFn fn_packed;  // packed-stage build (DD_CONFIG_PACKED_STAGES); nullptr if none
 };
 
-#define DDB_V(K, W) {K, W, 0, k_smem<K, W>, smem_max_threads<K, W>()}
-#define DDB_VI(K, W, I) {K, W, I, k_smem<K, W, I>, smem_max_threads<K, W>()}
+#define DDB_V(K, W) {K, W, 0, k_smem<K, W>, smem_max_threads<K, W>(), nullptr}
+#define DDB_VI(K, W, I) {K, W, I, k_smem<K, W, I>, smem_max_threads<K, W>(), nullptr}
+#define DDB_VP(K, W, I) \
+  {K, W, I, k_smem<K, W, I>, smem_max_threads<K, W>(), k_smem<K, W, I, true>}
 static const SmemVariant kSmemVariants[] = {
     DDB_V(1, 1),  DDB_V(1, 2),  DDB_V(1, 4),  DDB_V(1, 5),  DDB_V(1, 8),  DDB_V(1, 10),
     DDB_V(1, 16), DDB_V(1, 25), DDB_V(2, 1),  DDB_V(2, 2),  DDB_V(2, 4),  DDB_V(2, 5),
@@ -845,20 +874,25 @@ static const SmemVariant kSmemVariants[] = {
     DDB_V(8, 2),  DDB_V(8, 4),  DDB_V(8, 5),  DDB_V(8, 8),  DDB_V(16, 1), DDB_V(16, 2),
     DDB_V(16, 4),
     // compile-time items_time for the shapes the sweeps select (tuning/)
+    // (and packed-stage builds for the large-delay (LOFAR) shapes)
     DDB_VI(1, 5, 32), DDB_VI(2, 5, 32), DDB_VI(4, 5, 32), DDB_VI(1, 25, 8), DDB_VI(4, 10, 16),
-    DDB_VI(2, 5, 160), DDB_VI(1, 25, 64), DDB_VI(2, 25, 64), DDB_VI(4, 10, 160),
-    DDB_VI(2, 10, 160), DDB_VI(2, 25, 160),
+    DDB_VP(2, 5, 160), DDB_VP(1, 25, 64), DDB_VP(2, 25, 64), DDB_VP(4, 10, 160),
+    DDB_VP(2, 10, 160), DDB_VP(2, 25, 160),
 };
 #undef DDB_V
 #undef DDB_VI
+#undef DDB_VP
 
-KernelFn find_smem_kernel(uint32_t k, uint32_t w, uint32_t* max_threads, uint32_t items_time) {
+KernelFn find_smem_kernel(uint32_t k, uint32_t w, uint32_t* max_threads, uint32_t items_time,
+                          KernelFn* packed) {
   const SmemVariant* generic = nullptr;
+  if (packed) *packed = nullptr;
   for (const SmemVariant& v : kSmemVariants) {
     if (static_cast<uint32_t>(v.k) != k || static_cast<uint32_t>(v.w) != w) continue;
     if (v.it == 0 && generic == nullptr) generic = &v;
     if (items_time != 0 && static_cast<uint32_t>(v.it) == items_time) {
       if (max_threads) *max_threads = static_cast<uint32_t>(v.max_threads);
+      if (packed) *packed = v.fn_packed;
       return v.fn;
     }
   }

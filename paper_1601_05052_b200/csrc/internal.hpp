@@ -34,6 +34,7 @@ struct dd_plan {
   uint32_t* d_stage_ch = nullptr;   // packed stages: [stages + 1] first channels
   uint32_t* d_chan_off = nullptr;   // packed stages: [channels] window offsets
   void (*smem_fn)(const ddb::TiledArgs) = nullptr;
+  void (*smem_fn_fixed)(const ddb::TiledArgs) = nullptr;  // channel-range passes of a packed plan
   uint32_t blocks = 0, threads = 0, smem = 0;
   uint32_t grid_y = 1;
   uint32_t max_span = 0, max_delay = 0, group_span = 0, regwin_span = 0;
@@ -62,7 +63,7 @@ using KernelFn = void (*)(const TiledArgs);
 // instantiated.  *max_threads = the variant's block-size cap.
 // items_time != 0 selects a compile-time-stride build when one exists
 KernelFn find_smem_kernel(uint32_t k, uint32_t w, uint32_t* max_threads = nullptr,
-                          uint32_t items_time = 0);
+                          uint32_t items_time = 0, KernelFn* packed = nullptr);
 // Register-window variant for (work_dm, work_time) covering group_span
 // (or the widest one); *span_out = its SPAN.  nullptr when not instantiated.
 KernelFn find_regwin_kernel(uint32_t k, uint32_t w, uint32_t group_span, uint32_t* span_out);

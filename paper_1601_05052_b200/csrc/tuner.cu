@@ -194,6 +194,16 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
         c.flags = flags;
         v.push_back(c);
       }
+      // packed stages where a packed build exists (the large-delay shapes)
+      ddb::KernelFn packed = nullptr;
+      find_smem_kernel(k.work_dm, k.work_time, nullptr, k.items_time, &packed);
+      if (packed != nullptr) {
+        dd_config c = k;
+        c.dm_tile_depth = depth;
+        c.staging = DD_STAGING_SMEM;
+        c.flags = DD_CONFIG_PACKED_STAGES | DD_CONFIG_TIME_MAJOR;
+        v.push_back(c);
+      }
     }
     dd_config c = k;
     c.dm_tile_depth = 1;

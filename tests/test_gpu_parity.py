@@ -590,3 +590,43 @@ def test_every_gpu_space_config_is_bit_exact(dev, name, d):
         p.close()
     assert {"smem", "direct"} <= families
     assert rejected < len(space) // 4
+
+
+@pytest.mark.parametrize("cfg,depth", [(K(64, 4, 25, 1), 2), (K(160, 1, 10, 4), 1),
+                                       (K(64, 2, 25, 2), 1)])
+def test_packed_stages_bit_exact(dev, cfg, depth):
+    """DD_CONFIG_PACKED_STAGES on a wide-delay instance (LOFAR-like band):
+    stages packed by each channel's own window width -- full passes, beams
+    and (fixed-slot fallback) channel-range passes all reproduce the
+    reference."""
+    import torch
+    setup = api.ObservationSetup("packed", 3200, 16, 138.0, 0.19, 0.0, 25.0)
+    d = 32
+    table = api.build_delay_table(setup, d)
+    t = api.instance_sizing(setup, d).num_samples
+    s, c = setup.samples_per_second, setup.channels
+    fb = api.noise_filterbank(setup, t, 1.0, 44)
+    ref = O.dedisperse_reference(fb.data, table.shifts, s)
+    x = torch.from_numpy(fb.data).cuda()
+    sh = torch.from_numpy(table.shifts.view(np.int32)).cuda()
+    out = torch.full((d, s), float("nan"), device="cuda")
+    torch.cuda.synchronize()
+    p = dev.plan(sh.data_ptr(), c, d, s, t, t, cfg, depth, "smem",
+                 flags=N.DD_CONFIG_PACKED_STAGES | N.DD_CONFIG_TIME_MAJOR)
+    info = p.info()
+    assert info["packed_stages"] > 0 and info["packed_stages"] < c
+    p.execute(x.data_ptr(), out.data_ptr())
+    dev.synchronize()
+    assert np.array_equal(_bits(out.cpu().numpy()), _bits(ref))
+    out.fill_(float("nan"))
+    for i, (c0, c1) in enumerate([(0, 3), (3, 11), (11, 16)]):
+        p.execute_channels(x.data_ptr(), out.data_ptr(), c0, c1, accumulate=i > 0)
+    dev.synchronize()
+    assert np.array_equal(_bits(out.cpu().numpy()), _bits(ref))
+    xb = torch.stack([x, x * 2.0])
+    ob = torch.full((2, d, s), float("nan"), device="cuda")
+    torch.cuda.synchronize()
+    p.execute_beams(2, xb.data_ptr(), c * t, ob.data_ptr(), d * s)
+    dev.synchronize()
+    assert np.array_equal(_bits(ob[0].cpu().numpy()), _bits(ref))
+    assert np.array_equal(_bits(ob[1].cpu().numpy()), _bits(ref * 2.0))
