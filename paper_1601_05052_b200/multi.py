@@ -220,6 +220,56 @@ class ShardedDedisperser:
                     host_out[lo:hi].copy_(self.out[lo:hi], non_blocking=True)
         self.copy_stream.synchronize()
 
+    def stream_host(self, host_blocks, host_outs, steps: int) -> None:
+        """A survey's steady state: `steps` consecutive blocks, each through
+        the run_host(time) path, double-buffered on the device so block i+1's
+        H2D and kernels overlap block i's D2H (PCIe is full duplex; the D2H
+        of the output is the larger transfer).  Block i comes from
+        host_blocks[i % len(host_blocks)] and its rows land in
+        host_outs[i % 2] (pinned [count][s]); every block is copied in and
+        read back in full.  Single rank, h2d="time" (pipeline() first)."""
+        if self.world != 1 or self.h2d_mode != "time":
+            raise ValueError("stream_host needs a single rank and pipeline(h2d='time')")
+        if len(host_outs) != 2:
+            raise ValueError("stream_host needs two host output buffers")
+        if not hasattr(self, "_bufs"):
+            c, s = self.setup.channels, self.setup.samples_per_second
+            blk2 = torch.empty((c, self.pitch), dtype=torch.float32, device=self.device)
+            out2 = torch.empty((self.count, s), dtype=torch.float32, device=self.device)
+            self._bufs = [(self.block, self.out), (blk2, out2)]
+            n = len(self.chunks)
+            # per buffer: kernels done reading the block, D2H done per chunk
+            self._read_done = [torch.cuda.Event(), torch.cuda.Event()]
+            self._d2h_done = [[torch.cuda.Event() for _ in range(n)] for _ in range(2)]
+        t = self.num_samples
+        for i in range(steps):
+            b = i % 2
+            block, out = self._bufs[b]
+            hb, ho = host_blocks[i % len(host_blocks)], host_outs[b]
+            with torch.cuda.stream(self.h2d_stream):
+                if i >= 2:  # block b is free once step i-2's kernels are done
+                    self.h2d_stream.wait_event(self._read_done[b])
+                done_t = 0
+                for upto, ev in self.uploads:
+                    if upto > done_t:
+                        self.ctx.upload_block_range(hb.data_ptr(), t, block.data_ptr(),
+                                                    self.pitch, self.setup.channels, done_t,
+                                                    upto, self.h2d_stream.cuda_stream)
+                        done_t = upto
+                    ev.record(self.h2d_stream)
+            for j, ((lo, hi, plan, done), (_, ev)) in enumerate(zip(self.chunks, self.uploads)):
+                self.stream.wait_event(ev)
+                if i >= 2:  # rows lo:hi of out b have left for the host
+                    self.stream.wait_event(self._d2h_done[b][j])
+                plan.execute(block.data_ptr(), out[lo].data_ptr())
+                done.record(self.stream)
+                with torch.cuda.stream(self.copy_stream):
+                    self.copy_stream.wait_event(done)
+                    ho[lo:hi].copy_(out[lo:hi], non_blocking=True)
+                    self._d2h_done[b][j].record(self.copy_stream)
+            self._read_done[b].record(self.stream)
+        self.copy_stream.synchronize()
+
     def launch_order(self):
         """(channel group, DM chunk) kernel order for run_host.  No chunk can
         go D2H before the whole block is on the device, so the first

@@ -402,6 +402,21 @@ def test_sharded_driver_host_pipeline(dev, golden):
     dd.run()
     torch.cuda.synchronize()
     assert O.fnv1a(dd.out.cpu().numpy()) == g["out_fnv"]
+    # streamed consecutive blocks, double-buffered: the second block is the
+    # first times 2 (exact in fp32), so its output is the golden one times 2
+    ref = out.numpy().copy()
+    host2 = (host * 2).pin_memory()
+    outs = [torch.full_like(out, float("nan")).pin_memory() for _ in range(2)]
+    for steps in (5, 2):
+        for o in outs:
+            o.fill_(float("nan"))
+        dd.stream_host([host, host2], outs, steps)
+        torch.cuda.synchronize()
+        last = steps - 1
+        assert np.array_equal(_bits(outs[last % 2].numpy()),
+                              _bits(ref * (2 if last % 2 else 1)))
+        assert np.array_equal(_bits(outs[(last - 1) % 2].numpy()),
+                              _bits(ref * (2 if (last - 1) % 2 else 1)))
     # the TMEM family with GPU tiling, same pipeline
     dd2 = multi.ShardedDedisperser(setup, g["num_dms"], K(32, 4, 12, 8), 1, "tmem", device=0,
                                    gpu_tiling=True, stage_channels=8)
