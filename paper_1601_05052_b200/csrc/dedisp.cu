@@ -327,14 +327,23 @@ struct SmemBody {
 #pragma unroll
       for (int j = 0; j < W; ++j) acc[k][j] = 0.0f;
   }
+  // The K*W adds issue in pairs as FADD2 (flattened (k, j) order, two
+  // independent RN adds each: bit-exact), halving the FP32 instructions of
+  // the loop; an odd K*W leaves one scalar add.
   __device__ __forceinline__ void channel(const uint32_t* r, const float* w) {
     w += it;
+    const float* p[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const float* p = w + r[4 + id + k * a.items_dm];
+    for (int k = 0; k < K; ++k) p[k] = w + r[4 + id + k * a.items_dm];
 #pragma unroll
-      for (int j = 0; j < W; ++j) acc[k][j] += p[j * stride()];
+    for (int n = 0; n + 1 < K * W; n += 2) {
+      const int k0 = n / W, j0 = n % W, k1 = (n + 1) / W, j1 = (n + 1) % W;
+      const float2 s = fadd2(make_float2(acc[k0][j0], acc[k1][j1]),
+                             make_float2(p[k0][j0 * stride()], p[k1][j1 * stride()]));
+      acc[k0][j0] = s.x;
+      acc[k1][j1] = s.y;
     }
+    if ((K * W) & 1) acc[K - 1][W - 1] += p[K - 1][(W - 1) * stride()];
   }
   __device__ __forceinline__ void load(uint32_t dm0, uint32_t t0) {
 #pragma unroll

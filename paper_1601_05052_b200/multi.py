@@ -169,6 +169,7 @@ class ShardedDedisperser:
         self.groups = [(c * i // g, c * (i + 1) // g, torch.cuda.Event()) for i in range(g)]
         self.h2d_stream = torch.cuda.Stream(self.device)
         self.copy_stream = torch.cuda.Stream(self.device)
+        self._d2h_done = [[]]  # stream_host's per-chunk events follow the new cut
 
     def run_host(self, host_block: Optional[torch.Tensor], host_out: torch.Tensor) -> None:
         """End to end from host memory: the block's channel groups go H2D on
@@ -232,12 +233,13 @@ class ShardedDedisperser:
             raise ValueError("stream_host needs a single rank and pipeline(h2d='time')")
         if len(host_outs) != 2:
             raise ValueError("stream_host needs two host output buffers")
-        if not hasattr(self, "_bufs"):
+        n = len(self.chunks)
+        if getattr(self, "_bufs", None) is None:
             c, s = self.setup.channels, self.setup.samples_per_second
             blk2 = torch.empty((c, self.pitch), dtype=torch.float32, device=self.device)
             out2 = torch.empty((self.count, s), dtype=torch.float32, device=self.device)
             self._bufs = [(self.block, self.out), (blk2, out2)]
-            n = len(self.chunks)
+        if len(getattr(self, "_d2h_done", [[]])[0]) != n:  # pipeline() re-cut the chunks
             # per buffer: kernels done reading the block, D2H done per chunk
             self._read_done = [torch.cuda.Event(), torch.cuda.Event()]
             self._d2h_done = [[torch.cuda.Event() for _ in range(n)] for _ in range(2)]
