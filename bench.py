@@ -140,6 +140,12 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def workload_name(setup_name, c, s, t, d, world_size):
+    """The config.workload string both arms print (the same workload)."""
+    n = (2 if world_size == 1 else 4) if setup_name == "Apertif" else 3
+    return f"{setup_name} c={c} s={s} t={t}, {d} trial DMs, 1 s block (BASELINE config {n})"
+
+
 # ------------------------------------------------------- CPU baseline --
 class CpuBaseline:
     """The reference's tiled CPU kernel (ThreadPool over all host cores) on a
@@ -164,7 +170,7 @@ class CpuBaseline:
         while rows % (cfg[1] * cfg[3]):
             cfg = (cfg[0], 1, cfg[2], 1)
         self.cfg, self.rows, self.d, self.name = cfg, rows, d, setup_name
-        self.s = setup.samples_per_second
+        self.s, self.t, self.c = setup.samples_per_second, t, setup.channels
         self.flop = rows * self.s * setup.channels
         self.cores = os.cpu_count() or 1
         self.R = O.ref_lib()
@@ -221,7 +227,8 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(d * s * c / (v * 1e9) * 1e3, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.setup} d={d} (host CPU, reference dedisperse_tiled)"},
+            "config": {"workload": workload_name(args.setup, base.c, base.s, base.t, d, args.gpus),
+                       "path": "host CPU, reference dedisperse_tiled on a bounded DM sample"},
             "cpu_baseline": dict(samples[-1], value=round(v, 3)),
             "e2e": {"value": round(v, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -389,8 +396,7 @@ def run_ours(args):
             "data": "synthetic: noise_filterbank(sigma=1, seed=1) (the reference tuner's input), "
                     "device-built shift table",
             "config": {
-                "workload": f"{setup.name} c={c} s={s} t={t}, {d} trial DMs, 1 s block "
-                            f"(BASELINE config {2 if world_size == 1 else 4})",
+                "workload": workload_name(setup.name, c, s, t, d, world_size),
                 "kernel_config": {"items_time": cfgt[0], "items_dm": cfgt[1],
                                   "work_time": cfgt[2], "work_dm": cfgt[3],
                                   "dm_tile_depth": cfgt[4], "staging": cfgt[5],
