@@ -624,6 +624,10 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+#ifndef DDB_TMEM_GROUP
+#define DDB_TMEM_GROUP 4
+#endif
+
 template <int K, int W, int SPAN, int COLS, bool FULL_HEAD = true>
 struct TmemBody {
   static constexpr bool kRowBase = true;  // channel() gets the 16-byte aligned row start
@@ -752,12 +756,14 @@ struct TmemBody {
                                              const float* base) {
     if (fast) {
       // (ptxas schedules the loads itself: with the staging registers free
-      // between channels it keeps 3-4 of them in flight)
+      // between channels it keeps 3-4 of them in flight).  G DMs' TMEM reads
+      // per wait::ld (DDB_TMEM_GROUP, A/B builds).
+      constexpr int G = (DDB_TMEM_GROUP <= K && K % DDB_TMEM_GROUP == 0) ? DDB_TMEM_GROUP : 2;
 #pragma unroll
-      for (int k = 0; k < K; k += 2) {
-        float v[2][W];
+      for (int k = 0; k < K; k += G) {
+        float v[G][W];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < G; ++h) {
           const uint32_t c = taddr + off[k + h];
 #pragma unroll
           for (int j = 0; j + 8 <= W; j += 8) tmem_ld8(c + j, &v[h][j]);
@@ -765,7 +771,7 @@ struct TmemBody {
         }
         tmem_wait_ld();
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+        for (int h = 0; h < G; ++h)
 #pragma unroll
           for (int j = 0; j < W; j += 2) {
             const float2 s2 = fadd2(make_float2(acc[k + h][j], acc[k + h][j + 1]),
