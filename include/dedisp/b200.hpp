@@ -7,10 +7,15 @@
 // and exception types as the reference, so code written against the
 // reference compiles and behaves the same (bit-identical results).
 // Differences, all additive:
-//   * ExecOptions gains `device`, `dm_tile_depth` and `staging` (GPU knobs);
-//     `threads` and `pool` are accepted and ignored (the CUDA grid replaces
-//     the reference's ThreadPool).
-//   * TuningRecord carries the two GPU knobs next to the 4-tuple.
+//   * ExecOptions gains `device`, `dm_tile_depth`, `staging` and `flags`
+//     (GPU knobs); `threads` and `pool` are accepted and ignored (the CUDA
+//     grid replaces the reference's ThreadPool).  With the defaults
+//     (staging Auto, no flags) dedisperse_tiled validates the config by the
+//     reference's rules and then runs the instance's tuned schedule (the
+//     tuner's pick, register_schedule() or the built-in sweeps): every
+//     schedule computes the same bits, only faster.
+//   * TuningRecord carries the GPU knobs (depth, staging, flags, family)
+//     next to the 4-tuple, so a tuned record replays exactly.
 //   * device_error (a std::runtime_error) reports CUDA failures.
 //   * SIGPROC/raw file I/O, setup files, report/manifest JSON and the CLI
 //     are outside the hot path and not part of this library.
@@ -165,6 +170,7 @@ enum class Staging : std::uint32_t {
   SharedMemory = DD_STAGING_SMEM,
   Direct = DD_STAGING_DIRECT,
   RegisterWindow = DD_STAGING_REGWIN,
+  TensorMemory = DD_STAGING_TMEM,
 };
 
 struct ExecOptions {
@@ -175,6 +181,7 @@ struct ExecOptions {
   int device = 0;
   std::uint32_t dm_tile_depth = 1;
   Staging staging = Staging::Auto;
+  std::uint32_t flags = 0;       // DD_CONFIG_* (GPU tiling, stage shape, raster, ...)
 };
 
 bool config_valid(const KernelConfig& cfg, std::uint32_t num_dms, std::uint32_t samples_per_second,
@@ -207,6 +214,16 @@ struct TuningRecord {
   bool timer_warning = false;
   std::uint32_t dm_tile_depth = 1;
   Staging staging = Staging::Auto;
+  std::uint32_t flags = 0;   // DD_CONFIG_* the record was timed with
+  Staging family = Staging::Auto;  // kernel family that ran (staging Auto resolved)
+  // The ExecOptions that replay this record exactly.
+  ExecOptions exec_options() const {
+    ExecOptions o;
+    o.dm_tile_depth = dm_tile_depth;
+    o.staging = staging;
+    o.flags = flags;
+    return o;
+  }
 };
 
 struct TuningStats {
@@ -252,6 +269,7 @@ struct TuneOptions {
   int device = 0;
   bool full_reference_space = false;  // false: the GPU space (dd_enumerate_gpu_configs)
   std::uint32_t max_configs = 0;
+  bool flush_l2 = true;  // evict L2 before every timed run (cold-cache timing)
 };
 TuningResult tune(const ObservationSetup& setup, std::uint32_t num_dms,
                   const TuneOptions& options = {});
@@ -260,11 +278,17 @@ TuningResult zero_dm_experiment(const ObservationSetup& setup, std::uint32_t num
 
 struct FixedConfigReport {
   KernelConfig config;
+  std::uint32_t dm_tile_depth = 1;  // the GPU knobs of the fixed config
+  Staging staging = Staging::Auto;
+  std::uint32_t flags = 0;
   double total_gflops = 0.0;
   std::vector<double> fixed_gflops;
   std::vector<double> speedup_over_fixed;
 };
 FixedConfigReport best_fixed_config(std::span<const TuningResult> results);
+// The schedule dedisperse_tiled's Auto staging runs for the result's
+// instance from now on: its best record (dd_schedule_set).
+void register_schedule(const TuningResult& result);
 std::vector<std::uint32_t> default_instances();
 std::uint64_t estimate_instance_bytes(const ObservationSetup& setup, std::uint32_t num_dms);
 

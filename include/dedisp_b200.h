@@ -253,6 +253,10 @@ dd_status dd_plan_execute_beams(dd_plan* plan, uint32_t beams, const float* d_in
  * receives each run. */
 dd_status dd_plan_time(dd_plan* plan, const float* d_in, float* d_out, uint64_t out_pitch,
                        uint32_t warmup, uint32_t repeats, double* seconds);
+/* As dd_plan_time; flush_l2 = 1 overwrites a context buffer of twice the
+ * L2 size before every timed run, outside the events (cold-L2 timing). */
+dd_status dd_plan_time_ex(dd_plan* plan, const float* d_in, float* d_out, uint64_t out_pitch,
+                          uint32_t warmup, uint32_t repeats, int flush_l2, double* seconds);
 
 /* One-shot device-buffer dedispersion: plan + execute + destroy. */
 dd_status dd_dedisperse_device(dd_context* ctx, const float* d_in, uint32_t channels,
@@ -265,7 +269,15 @@ dd_status dd_dedisperse_device(dd_context* ctx, const float* d_in, uint32_t chan
  * kernels.cpp:83-108) and dedisperse_tiled_into (kernels.cpp:117-206):
  * checks the pair (kernels.cpp:16-28), validates cfg against the reference
  * limits, uploads, runs, downloads h_out (num_dms x samples_per_second).
- * Synchronous. */
+ * Synchronous.  The context keeps the device buffers and the last plan
+ * between calls (the plan is reused while the table and config repeat).
+ *
+ * Tuned dispatch (dd_dedisperse and dd_dedisperse_device): a config with
+ * staging DD_STAGING_AUTO and no flags is validated by the reference's
+ * rules, then the instance's tuned schedule (dd_schedule_get) runs in its
+ * place when one exists -- every schedule computes the same bits (one fp32
+ * accumulator per output, channels ascending), so only the speed changes.
+ * If the schedule cannot be planned for this table the config itself runs. */
 dd_status dd_dedisperse(dd_context* ctx, const float* h_in, uint32_t channels,
                         uint64_t num_samples, const uint32_t* h_shifts, uint32_t num_dms,
                         uint32_t samples_per_second, const dd_config* cfg,
@@ -293,6 +305,29 @@ dd_status dd_upload_block_range(dd_context* ctx, const float* h_block, uint64_t 
                                 float* d_block, uint64_t d_pitch, uint32_t channels,
                                 uint64_t t0, uint64_t t1, void* stream);
 
+/* --------------------------------------------------- tuned schedules -- */
+/* The configuration the one-shot entry points run for an AUTO config on an
+ * instance of `channels` channels, `samples_per_second` and `num_dms`
+ * trials: one registered with dd_schedule_set (e.g. a tuning result's best
+ * record, tuner.cpp:172-179), else a built-in pick from the committed
+ * sweeps (tuning/, Apertif- and LOFAR-like geometries, d = 2..4096).
+ * dd_schedule_get returns DD_ERR_INVALID_ARGUMENT when there is none;
+ * *builtin (may be NULL) tells which table answered. */
+dd_status dd_schedule_set(uint32_t channels, uint32_t samples_per_second, uint32_t num_dms,
+                          const dd_config* cfg); /* cfg == NULL forgets the entry */
+dd_status dd_schedule_get(uint32_t channels, uint32_t samples_per_second, uint32_t num_dms,
+                          dd_config* cfg, int* builtin);
+/* The schedule the last dd_dedisperse / dd_dedisperse_device on this
+ * context actually ran (the tuned one, or the caller's config). */
+dd_status dd_last_run_config(dd_context* ctx, dd_config* cfg, uint32_t* family);
+
+/* ------------------------------------------------------ fingerprints -- */
+/* FNV-1a 64 (basis 0xcbf29ce484222325, prime 0x100000001b3) over `bytes`
+ * bytes of host memory: the fingerprint the golden fixtures use
+ * (tests/golden/golden.json), so a caller can check a full output against
+ * the reference's without keeping the reference's output around. */
+dd_status dd_fingerprint(const void* data, uint64_t bytes, uint64_t* out);
+
 /* ---------------------------------------------- synthetic input ------- */
 /* noise_filterbank, filterbank.cpp:60-80: mt19937_64(seed), Box-Muller,
  * channel-major fill, float(sigma * g).  Host memory; threads = 0 -> all. */
@@ -315,6 +350,13 @@ typedef struct dd_tune_options {
                              kernels support, x depth x staging);
                              1: the full reference divisor space */
   uint32_t max_configs;   /* 0 = no cap */
+  uint32_t flush_l2;      /* 1: write a buffer larger than L2 before every
+                             timed run (outside the events), so instances
+                             whose input fits the 126 MB L2 are timed cold */
+  uint32_t reserved;
+  double* runs;           /* NULL, or repeats doubles per record (record
+                             order): every timed run in seconds, the
+                             reference's runs_s (report_io.cpp:70-79) */
 } dd_tune_options;
 
 /* The GPU tuning space for an instance (see dd_tune_options.space = 0). */

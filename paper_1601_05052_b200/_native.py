@@ -69,7 +69,9 @@ class dd_plan_info(C.Structure):
 
 class dd_tune_options(C.Structure):
     _fields_ = [("limits", dd_limits), ("repeats", C.c_uint32), ("zero_dm", C.c_uint32),
-                ("seed", C.c_uint64), ("space", C.c_uint32), ("max_configs", C.c_uint32)]
+                ("seed", C.c_uint64), ("space", C.c_uint32), ("max_configs", C.c_uint32),
+                ("flush_l2", C.c_uint32), ("reserved", C.c_uint32),
+                ("runs", C.POINTER(C.c_double))]
 
 
 class dd_tuning_record(C.Structure):
@@ -124,6 +126,11 @@ SIGNATURES = {
     "dd_plan_get_info": (i32, [P, C.POINTER(dd_plan_info)]),
     "dd_plan_execute": (i32, [P, P, P, u64]),
     "dd_plan_time": (i32, [P, P, P, u64, u32, u32, pdbl]),
+    "dd_plan_time_ex": (i32, [P, P, P, u64, u32, u32, C.c_int, pdbl]),
+    "dd_fingerprint": (i32, [P, u64, pu64]),
+    "dd_schedule_set": (i32, [u32, u32, u32, C.POINTER(dd_config)]),
+    "dd_schedule_get": (i32, [u32, u32, u32, C.POINTER(dd_config), C.POINTER(C.c_int)]),
+    "dd_last_run_config": (i32, [P, C.POINTER(dd_config), pu32]),
     "dd_plan_execute_channels": (i32, [P, P, P, u64, u32, u32, C.c_int]),
     "dd_plan_execute_beams": (i32, [P, u32, P, u64, P, u64, u64]),
     "dd_dedisperse_device": (i32, [P, P, u32, u64, u64, P, u32, u32, C.POINTER(dd_config),

@@ -352,6 +352,12 @@ class Context:
             lib().dd_context_destroy(self.handle)
             self.handle = C.c_void_p()
 
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
     def set_stream(self, stream_ptr: int) -> None:
         check(lib().dd_context_set_stream(self.handle, C.c_void_p(stream_ptr or None)))
 
@@ -461,10 +467,12 @@ class Plan:
                                           out_beam_stride))
 
     def time(self, d_in: int, d_out: int, warmup: int = 1, repeats: int = 10,
-             out_pitch: Optional[int] = None) -> List[float]:
+             out_pitch: Optional[int] = None, flush_l2: bool = False) -> List[float]:
+        """CUDA-event time of each of `repeats` runs after `warmup` untimed
+        ones; flush_l2 evicts L2 before every timed run (outside the events)."""
         runs = (C.c_double * max(repeats, 1))()
-        check(lib().dd_plan_time(self.handle, C.c_void_p(d_in), C.c_void_p(d_out),
-                                 out_pitch or self.s, warmup, repeats, runs))
+        check(lib().dd_plan_time_ex(self.handle, C.c_void_p(d_in), C.c_void_p(d_out),
+                                    out_pitch or self.s, warmup, repeats, int(flush_l2), runs))
         return list(runs[:repeats])
 
 
@@ -594,9 +602,11 @@ def _stats(s) -> TuningStats:
                        None if deg else s.chebyshev_bound, deg)
 
 
-def _sweep(setup, num_dms, limits, repeats, seed, zero, full_space, max_configs, device):
+def _sweep(setup, num_dms, limits, repeats, seed, zero, full_space, max_configs, device,
+           flush_l2=True):
     ctx = context(device)
-    opt = N.dd_tune_options(limits.c(), repeats, int(zero), seed, int(full_space), max_configs)
+    opt = N.dd_tune_options(limits.c(), repeats, int(zero), seed, int(full_space), max_configs,
+                            int(flush_l2), 0)
     n = C.c_uint64()
     if full_space:
         check(lib().dd_enumerate_configs(num_dms, setup.samples_per_second, C.byref(limits.c()),
@@ -604,15 +614,20 @@ def _sweep(setup, num_dms, limits, repeats, seed, zero, full_space, max_configs,
     else:
         check(lib().dd_enumerate_gpu_configs(ctx.handle, C.byref(setup.c()), num_dms,
                                              C.byref(limits.c()), None, 0, C.byref(n)))
+    if max_configs:
+        n.value = min(n.value, max_configs)
     recs = (N.dd_tuning_record * max(n.value, 1))()
+    runs = (C.c_double * max(n.value * repeats, 1))()
+    opt.runs = C.cast(runs, C.POINTER(C.c_double))
     summ = N.dd_tuning_summary()
     check(lib().dd_tune(ctx.handle, C.byref(setup.c()), num_dms, C.byref(opt), recs, n.value,
                         C.byref(summ)))
     out = []
-    for r in recs[:summ.count]:
+    for i, r in enumerate(recs[:summ.count]):
         k = r.config
         out.append(TuningRecord(KernelConfig(k.items_time, k.items_dm, k.work_time, k.work_dm),
-                                [], r.mean_time, r.gflops, bool(r.timer_warning),
+                                list(runs[i * repeats:(i + 1) * repeats]), r.mean_time,
+                                r.gflops, bool(r.timer_warning),
                                 k.dm_tile_depth, N.STAGING_NAME[k.staging],
                                 N.STAGING_NAME.get(r.family, ""), k.flags))
     return TuningResult(setup, num_dms, zero, limits, repeats, seed, out, summ.best_index,
@@ -621,18 +636,65 @@ def _sweep(setup, num_dms, limits, repeats, seed, zero, full_space, max_configs,
 
 def tune(setup: ObservationSetup, num_dms: int, limits: KernelLimits = KernelLimits(),
          repeats: int = 10, seed: int = 1, full_reference_space: bool = False,
-         max_configs: int = 0, device: int = 0) -> TuningResult:
-    """reference tuner.cpp:208-211 on the device (CUDA-event timing)."""
+         max_configs: int = 0, device: int = 0, flush_l2: bool = True) -> TuningResult:
+    """reference tuner.cpp:208-211 on the device (CUDA-event timing; L2
+    flushed before every timed run unless flush_l2=False; every run kept in
+    record.runs like the reference's runs_s)."""
     return _sweep(setup, num_dms, limits, repeats, seed, False, full_reference_space,
-                  max_configs, device)
+                  max_configs, device, flush_l2)
 
 
 def zero_dm_experiment(setup: ObservationSetup, num_dms: int, limits: KernelLimits = KernelLimits(),
                        repeats: int = 10, seed: int = 1, full_reference_space: bool = False,
-                       max_configs: int = 0, device: int = 0) -> TuningResult:
+                       max_configs: int = 0, device: int = 0,
+                       flush_l2: bool = True) -> TuningResult:
     """reference tuner.cpp:213-216"""
     return _sweep(setup, num_dms, limits, repeats, seed, True, full_reference_space,
-                  max_configs, device)
+                  max_configs, device, flush_l2)
+
+
+def schedule_set(channels: int, samples_per_second: int, num_dms: int,
+                 record: Optional["TuningRecord"]) -> None:
+    """Register the schedule the one-shot entry points (dedisperse_tiled with
+    staging "auto") run for this instance -- typically a tuning result's
+    best record; None forgets it (dd_schedule_set)."""
+    if record is None:
+        check(lib().dd_schedule_set(channels, samples_per_second, num_dms, None))
+        return
+    kc = _cfg(record.config, record.dm_tile_depth, record.staging)
+    kc.flags = record.flags
+    check(lib().dd_schedule_set(channels, samples_per_second, num_dms, C.byref(kc)))
+
+
+def schedule_get(channels: int, samples_per_second: int, num_dms: int):
+    """(KernelConfig, dm_tile_depth, staging, flags, builtin) of the
+    instance's tuned schedule, or None (dd_schedule_get)."""
+    kc, b = N.dd_config(), C.c_int()
+    if lib().dd_schedule_get(channels, samples_per_second, num_dms, C.byref(kc),
+                             C.byref(b)) != N.DD_OK:
+        return None
+    return (KernelConfig(kc.items_time, kc.items_dm, kc.work_time, kc.work_dm), kc.dm_tile_depth,
+            N.STAGING_NAME[kc.staging], kc.flags, bool(b.value))
+
+
+def last_run_config(device: int = 0):
+    """What the last one-shot call on this device's context ran:
+    (KernelConfig, dm_tile_depth, staging, flags, family)."""
+    kc, fam = N.dd_config(), C.c_uint32()
+    check(lib().dd_last_run_config(context(device).handle, C.byref(kc), C.byref(fam)))
+    return (KernelConfig(kc.items_time, kc.items_dm, kc.work_time, kc.work_dm), kc.dm_tile_depth,
+            N.STAGING_NAME[kc.staging], kc.flags, N.STAGING_NAME.get(fam.value, fam.value))
+
+
+def fingerprint(a) -> str:
+    """FNV-1a 64 of an array's raw bytes (dd_fingerprint), the hash the
+    golden fixtures use; a host numpy array or anything with .numpy()."""
+    if hasattr(a, "numpy"):
+        a = a.numpy()
+    a = np.ascontiguousarray(a)
+    h = C.c_uint64()
+    check(lib().dd_fingerprint(a.ctypes.data, a.nbytes, C.byref(h)))
+    return "%016x" % h.value
 
 
 @dataclass

@@ -9,6 +9,10 @@
 #include <string>
 #include <vector>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "internal.hpp"
 
 namespace ddb {
@@ -135,6 +139,11 @@ dd_status dd_context_destroy(dd_context* c) {
   cudaStreamSynchronize(c->stream);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   cudaFree(c->d_scratch);
+  cudaFree(c->d_flush);
+  dd_plan_destroy(c->cached_plan);
+  cudaFree(c->d_in);
+  cudaFree(c->d_sh);
+  cudaFree(c->d_out);
   cudaEventDestroy(c->ev_start);
   cudaEventDestroy(c->ev_stop);
   delete c;
@@ -505,7 +514,10 @@ void free_plan_buffers(dd_plan* p) {
 cudaError_t pack_stages(dd_context* c, dd_plan* p, ddb::TiledArgs& a, uint32_t channels,
                         uint32_t slack, uint32_t flags, uint32_t* smem) {
   std::vector<uint32_t> span(channels);
-  cudaError_t e = cudaMemcpy(span.data(), p->d_chan_span, channels * 4, cudaMemcpyDeviceToHost);
+  // on the context stream (which k_plan wrote d_chan_span on), then wait
+  cudaError_t e = cudaMemcpyAsync(span.data(), p->d_chan_span, channels * 4,
+                                  cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return e;
   const uint32_t want_ns = (flags & DD_CONFIG_NSTAGE_MASK) >> DD_CONFIG_NSTAGE_SHIFT;
   const uint32_t ns = want_ns >= 2 ? want_ns : 2;
@@ -530,9 +542,15 @@ cudaError_t pack_stages(dd_context* c, dd_plan* p, ddb::TiledArgs& a, uint32_t c
   stage_ch.push_back(channels);
   e = cudaMalloc(&p->d_stage_ch, stage_ch.size() * 4);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_chan_off, channels * 4);
+  // pageable sources: async on the context stream, then wait so the host
+  // vectors may die and the first launch on that stream sees the tables
   if (e == cudaSuccess)
-    e = cudaMemcpy(p->d_stage_ch, stage_ch.data(), stage_ch.size() * 4, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(p->d_chan_off, off.data(), channels * 4, cudaMemcpyHostToDevice);
+    e = cudaMemcpyAsync(p->d_stage_ch, stage_ch.data(), stage_ch.size() * 4,
+                        cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(p->d_chan_off, off.data(), channels * 4, cudaMemcpyHostToDevice,
+                        c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return e;
   a.packed = 1;
   a.packed_stages = static_cast<uint32_t>(stage_ch.size() - 1);
@@ -544,7 +562,6 @@ cudaError_t pack_stages(dd_context* c, dd_plan* p, ddb::TiledArgs& a, uint32_t c
   *smem = static_cast<uint32_t>(fixed - static_cast<uint64_t>(ns) * (ddb::kMaxCps - widest) *
                                             a.rec_bytes +
                                 4ull * ns * stage_floats);
-  (void)c;
   return cudaSuccess;
 }
 
@@ -948,11 +965,25 @@ dd_status dd_plan_execute_beams(dd_plan* p, uint32_t beams, const float* d_in,
 
 dd_status dd_plan_time(dd_plan* p, const float* d_in, float* d_out, uint64_t out_pitch,
                        uint32_t warmup, uint32_t repeats, double* seconds) {
+  return dd_plan_time_ex(p, d_in, d_out, out_pitch, warmup, repeats, 0, seconds);
+}
+
+dd_status dd_plan_time_ex(dd_plan* p, const float* d_in, float* d_out, uint64_t out_pitch,
+                          uint32_t warmup, uint32_t repeats, int flush_l2, double* seconds) {
   if (p == nullptr || (repeats > 0 && seconds == nullptr))
     return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
   dd_context* c = p->ctx;
+  DD_CUDA(cudaSetDevice(c->device));
+  if (flush_l2 && c->d_flush == nullptr) {
+    const uint64_t bytes = std::max<uint64_t>(2ull * static_cast<uint64_t>(c->l2_bytes), 64ull << 20);
+    DD_CUDA(cudaMalloc(&c->d_flush, bytes));
+    c->flush_bytes = bytes;
+  }
   for (uint32_t i = 0; i < warmup; ++i) DD_TRY(dd_plan_execute(p, d_in, d_out, out_pitch));
   for (uint32_t i = 0; i < repeats; ++i) {
+    // evict the instance from L2 outside the timed region (a memset of a
+    // buffer twice the L2 size), as bench.py does between its steps
+    if (flush_l2) DD_CUDA(cudaMemsetAsync(c->d_flush, i & 0xff, c->flush_bytes, c->stream));
     DD_CUDA(cudaEventRecord(c->ev_start, c->stream));
     DD_TRY(dd_plan_execute(p, d_in, d_out, out_pitch));
     DD_CUDA(cudaEventRecord(c->ev_stop, c->stream));
@@ -965,15 +996,136 @@ dd_status dd_plan_time(dd_plan* p, const float* d_in, float* d_out, uint64_t out
   return DD_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// ------------------------------------------------------ tuned schedules --
+struct BuiltinSchedule {
+  uint32_t channels, s, num_dms;
+  dd_config cfg;
+};
+const BuiltinSchedule kBuiltinSchedules[] = {
+#include "schedules.inc"
+};
+
+using ScheduleKey = std::tuple<uint32_t, uint32_t, uint32_t>;
+std::mutex g_sched_mu;
+std::map<ScheduleKey, dd_config>& registered() {
+  static std::map<ScheduleKey, dd_config> m;
+  return m;
+}
+
+// The config the one-shot entry points plan: the instance's tuned schedule
+// for an AUTO, flag-free config (the reference API's default ExecOptions),
+// else the caller's own.
+bool tuned_for(const dd_config* k, uint32_t channels, uint32_t s, uint32_t num_dms,
+               dd_config* out) {
+  if (k == nullptr || k->staging != DD_STAGING_AUTO || k->flags != 0) return false;
+  int builtin = 0;
+  if (dd_schedule_get(channels, s, num_dms, out, &builtin) != DD_OK) {
+    clear_error();
+    return false;
+  }
+  return true;
+}
+
+// Plan the tuned schedule when there is one (validated against the default
+// limits: it is the library's choice, not the caller's), else -- or when the
+// schedule cannot be planned for this table -- the caller's config.
+dd_status plan_one_shot(dd_context* c, const uint32_t* d_shifts, uint32_t channels,
+                        uint32_t num_dms, uint32_t s, uint64_t num_samples, uint64_t pitch,
+                        const dd_config* k, const dd_limits* limits, dd_plan** p,
+                        dd_config* ran) {
+  dd_config tuned{};
+  if (tuned_for(k, channels, s, num_dms, &tuned)) {
+    const dd_status st =
+        dd_plan_create(c, d_shifts, channels, num_dms, s, num_samples, pitch, &tuned, nullptr, p);
+    if (st == DD_OK) {
+      *ran = tuned;
+      return DD_OK;
+    }
+    if (st != DD_ERR_INVALID_ARGUMENT) return st;
+    clear_error();
+  }
+  DD_TRY(dd_plan_create(c, d_shifts, channels, num_dms, s, num_samples, pitch, k, limits, p));
+  *ran = k ? *k : dd_config{};
+  return DD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+dd_status dd_schedule_set(uint32_t channels, uint32_t s, uint32_t num_dms, const dd_config* cfg) {
+  if (channels == 0 || s == 0 || num_dms == 0)
+    return fail(DD_ERR_INVALID_ARGUMENT, "instance dimensions must be positive");
+  std::lock_guard<std::mutex> g(g_sched_mu);
+  if (cfg == nullptr) {
+    registered().erase(ScheduleKey{channels, s, num_dms});
+    return DD_OK;
+  }
+  DD_TRY(dd_validate_config(cfg, num_dms, s, nullptr));
+  registered()[ScheduleKey{channels, s, num_dms}] = *cfg;
+  return DD_OK;
+}
+
+dd_status dd_schedule_get(uint32_t channels, uint32_t s, uint32_t num_dms, dd_config* cfg,
+                          int* builtin) {
+  if (cfg == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "cfg is null");
+  {
+    std::lock_guard<std::mutex> g(g_sched_mu);
+    auto it = registered().find(ScheduleKey{channels, s, num_dms});
+    if (it != registered().end()) {
+      *cfg = it->second;
+      if (builtin) *builtin = 0;
+      return DD_OK;
+    }
+  }
+  for (const BuiltinSchedule& b : kBuiltinSchedules)
+    if (b.channels == channels && b.s == s && b.num_dms == num_dms) {
+      *cfg = b.cfg;
+      if (builtin) *builtin = 1;
+      return DD_OK;
+    }
+  return fail(DD_ERR_INVALID_ARGUMENT, "no tuned schedule for this instance");
+}
+
+dd_status dd_last_run_config(dd_context* c, dd_config* cfg, uint32_t* family) {
+  if (c == nullptr || cfg == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  *cfg = c->last_run;
+  if (family) *family = c->last_family;
+  return DD_OK;
+}
+
 dd_status dd_dedisperse_device(dd_context* c, const float* d_in, uint32_t channels,
                                uint64_t num_samples, uint64_t in_pitch, const uint32_t* d_shifts,
                                uint32_t num_dms, uint32_t s, const dd_config* k,
                                const dd_limits* limits, float* d_out) {
+  if (c == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "context is null");
+  if (k != nullptr) DD_TRY(dd_validate_config(k, num_dms, s, limits));
   dd_plan* p = nullptr;
-  DD_TRY(dd_plan_create(c, d_shifts, channels, num_dms, s, num_samples, in_pitch, k, limits, &p));
+  dd_config ran{};
+  DD_TRY(plan_one_shot(c, d_shifts, channels, num_dms, s, num_samples, in_pitch, k, limits, &p,
+                       &ran));
+  c->last_run = ran;
+  c->last_family = p->family;
   dd_status st = dd_plan_execute(p, d_in, d_out, s);
   dd_plan_destroy(p);
   return st;
+}
+
+dd_status dd_fingerprint(const void* data, uint64_t bytes, uint64_t* out) {
+  if (out == nullptr || (data == nullptr && bytes != 0))
+    return fail(DD_ERR_INVALID_ARGUMENT, "null argument");
+  const unsigned char* b = static_cast<const unsigned char*>(data);
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (uint64_t i = 0; i < bytes; ++i) {
+    h ^= b[i];
+    h *= 0x100000001b3ull;
+  }
+  *out = h;
+  return DD_OK;
 }
 
 // Host-buffer drop-in for dedisperse_reference_into / dedisperse_tiled_into.
@@ -995,26 +1147,58 @@ dd_status dd_dedisperse(dd_context* c, const float* h_in, uint32_t channels, uin
   if (k != nullptr) DD_TRY(dd_validate_config(k, num_dms, s, limits));
   DD_CUDA(cudaSetDevice(c->device));
   const uint64_t pitch = (num_samples + 3) & ~3ull;
-  void *d_in = nullptr, *d_sh = nullptr, *d_out = nullptr;
-  dd_status st = dd_device_malloc(c, pitch * channels * 4, &d_in);
-  if (st == DD_OK) st = dd_device_malloc(c, entries * 4, &d_sh);
-  if (st == DD_OK) st = dd_device_malloc(c, static_cast<uint64_t>(num_dms) * s * 4, &d_out);
-  if (st == DD_OK)
-    st = dd_upload_filterbank(c, static_cast<float*>(d_in), pitch, h_in, channels, num_samples);
-  if (st == DD_OK) st = dd_copy_h2d(c, d_sh, h_shifts, entries * 4);
-  if (st == DD_OK)
-    st = dd_dedisperse_device(c, static_cast<float*>(d_in), channels, num_samples, pitch,
-                              static_cast<uint32_t*>(d_sh), num_dms, s, k, limits,
-                              static_cast<float*>(d_out));
-  if (st == DD_OK) st = dd_copy_d2h(c, h_out, d_out, static_cast<uint64_t>(num_dms) * s * 4);
-  if (st == DD_OK) {
-    const cudaError_t e = cudaStreamSynchronize(c->stream);
-    if (e != cudaSuccess) st = cuda_fail(e, "dd_dedisperse");
+  const uint64_t in_bytes = pitch * channels * 4, sh_bytes = entries * 4;
+  const uint64_t out_bytes = static_cast<uint64_t>(num_dms) * s * 4;
+  // device buffers kept on the context across calls (grown when needed; a
+  // new table buffer invalidates the cached plan, which points into it)
+  auto grow = [&](void** buf, uint64_t* cap, uint64_t need) -> dd_status {
+    if (*cap >= need) return DD_OK;
+    DD_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    DD_TRY(dd_device_malloc(c, need, buf));
+    *cap = need;
+    return DD_OK;
+  };
+  const void* old_sh = c->d_sh;
+  DD_TRY(grow(&c->d_in, &c->in_cap, in_bytes));
+  DD_TRY(grow(&c->d_sh, &c->sh_cap, sh_bytes));
+  DD_TRY(grow(&c->d_out, &c->out_cap, out_bytes));
+  // the plan (pre-pass, shared-memory sizing) is reused while the table and
+  // the request repeat -- a tuner or a survey calls with the same table
+  const uint64_t key[8] = {channels, num_samples, num_dms, s,
+                           k ? (uint64_t{k->items_time} << 32 | k->items_dm) : ~0ull,
+                           k ? (uint64_t{k->work_time} << 32 | k->work_dm) : ~0ull,
+                           k ? (uint64_t{k->dm_tile_depth} << 32 | k->staging) : ~0ull,
+                           (k ? uint64_t{k->flags} : ~0ull) ^
+                               (limits ? (uint64_t{limits->max_block_items} << 32 |
+                                          limits->max_accumulators) << 8
+                                       : 0)};
+  const bool same = c->cached_plan != nullptr && old_sh == c->d_sh &&
+                    std::memcmp(key, c->cached_key, sizeof(key)) == 0 &&
+                    c->cached_table.size() == entries &&
+                    std::memcmp(c->cached_table.data(), h_shifts, sh_bytes) == 0;
+  if (!same) {
+    dd_plan_destroy(c->cached_plan);
+    c->cached_plan = nullptr;
+    c->cached_table.clear();
+    DD_TRY(dd_copy_h2d(c, c->d_sh, h_shifts, sh_bytes));
+    dd_config ran{};
+    DD_TRY(plan_one_shot(c, static_cast<uint32_t*>(c->d_sh), channels, num_dms, s, num_samples,
+                         pitch, k, limits, &c->cached_plan, &ran));
+    c->cached_table.assign(h_shifts, h_shifts + entries);
+    std::memcpy(c->cached_key, key, sizeof(key));
+    c->last_run = ran;
+    c->last_family = c->cached_plan->family;
   }
-  cudaFree(d_in);
-  cudaFree(d_sh);
-  cudaFree(d_out);
-  return st;
+  DD_TRY(dd_upload_filterbank(c, static_cast<float*>(c->d_in), pitch, h_in, channels,
+                              num_samples));
+  DD_TRY(dd_plan_execute(c->cached_plan, static_cast<float*>(c->d_in),
+                         static_cast<float*>(c->d_out), s));
+  DD_TRY(dd_copy_d2h(c, h_out, c->d_out, out_bytes));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  return DD_OK;
 }
 
 }  // extern "C"

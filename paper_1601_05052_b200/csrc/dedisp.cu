@@ -781,9 +781,12 @@ struct TmemBody {
           }
       }
     } else {
+      // slow path (a group with a DM below its first): k_plan's window
+      // offsets are relative to the first DM's aligned start and wrap below
+      // it, so they are applied as signed 32-bit displacements
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        const float* q = base + off[k];
+        const float* q = base + static_cast<int32_t>(off[k]);
 #pragma unroll
         for (int j = 0; j < W; ++j) acc[k][j] += q[j];
       }

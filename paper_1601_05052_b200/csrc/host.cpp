@@ -47,8 +47,10 @@ dd_setup to_c(const ObservationSetup& s) {
 }
 
 dd_config to_c(const KernelConfig& k, const ExecOptions& o) {
-  return dd_config{k.items_time, k.items_dm,           k.work_time,
-                   k.work_dm,    o.dm_tile_depth,      static_cast<uint32_t>(o.staging)};
+  return dd_config{k.items_time,     k.items_dm,
+                   k.work_time,      k.work_dm,
+                   o.dm_tile_depth,  static_cast<uint32_t>(o.staging),
+                   o.flags};
 }
 
 dd_limits to_c(const KernelLimits& l) { return dd_limits{l.max_block_items, l.max_accumulators}; }
@@ -194,17 +196,22 @@ DedispersedSeries dedisperse_reference(const Filterbank& fb, const DelayTable& t
 void dedisperse_tiled_into(DedispersedSeries& out, const Filterbank& fb, const DelayTable& table,
                            const KernelConfig& cfg, const ExecOptions& options) {
   check_pair(fb, table);
-  validate_config(cfg, table.num_dms, fb.setup.samples_per_second, options.limits);
+  // the reference's rules (kernels.cpp:58-81); GPU flags in the options
+  // (a replayed tuning record) relax only what they name
   const dd_config c = to_c(cfg, options);
   const dd_limits l = to_c(options.limits);
+  check(dd_validate_config(&c, table.num_dms, fb.setup.samples_per_second, &l));
   run(out, fb, table, &c, &l, options.device);
   if (options.stats != nullptr) {
     options.stats->flop_additions.fetch_add(
         static_cast<std::uint64_t>(table.num_dms) * fb.setup.samples_per_second * fb.setup.channels,
         std::memory_order_relaxed);
-    options.stats->staged_loads.fetch_add(
-        count_loads(table, cfg, table.num_dms, fb.setup.samples_per_second).staged_loads,
-        std::memory_order_relaxed);
+    // count_loads.cpp:9-68 for the config as given (a GPU-tiled one counts
+    // its predicated last tile like a full one)
+    std::uint64_t staged = 0, ideal = 0;
+    check(dd_count_loads(table.shifts.data(), table.setup.channels, table.num_dms,
+                         fb.setup.samples_per_second, &c, &staged, &ideal));
+    options.stats->staged_loads.fetch_add(staged, std::memory_order_relaxed);
   }
 }
 
@@ -248,14 +255,15 @@ TuningRecord benchmark_config(const Filterbank& fb, const DelayTable& table,
                               const ExecOptions& options) {
   if (repeats == 0) throw std::invalid_argument("need at least one timed repeat");
   check_pair(fb, table);
-  validate_config(cfg, table.num_dms, fb.setup.samples_per_second, options.limits);
   const std::uint32_t d = table.num_dms, s = fb.setup.samples_per_second, c = fb.setup.channels;
   const dd_config kc = to_c(cfg, options);
   const dd_limits l = to_c(options.limits);
+  check(dd_validate_config(&kc, d, s, &l));
   TuningRecord rec;
   rec.config = cfg;
   rec.dm_tile_depth = options.dm_tile_depth;
   rec.staging = options.staging;
+  rec.flags = options.flags;
   rec.runs.resize(repeats);
 
   std::lock_guard<std::mutex> g(g_mu);
@@ -276,6 +284,10 @@ TuningRecord benchmark_config(const Filterbank& fb, const DelayTable& table,
   if (st == DD_OK)
     st = dd_plan_time(plan, static_cast<float*>(din), static_cast<float*>(dout), s, 1, repeats,
                       rec.runs.data());
+  if (st == DD_OK) {
+    dd_plan_info info{};
+    if (dd_plan_get_info(plan, &info) == DD_OK) rec.family = static_cast<Staging>(info.family);
+  }
   dd_plan_destroy(plan);
   dd_device_free(ctx, din);
   dd_device_free(ctx, dsh);
@@ -294,9 +306,11 @@ namespace {
 dd_tuning_record to_c(const TuningRecord& r) {
   dd_tuning_record c{};
   c.config = dd_config{r.config.items_time, r.config.items_dm, r.config.work_time,
-                       r.config.work_dm, r.dm_tile_depth, static_cast<uint32_t>(r.staging)};
+                       r.config.work_dm,    r.dm_tile_depth,   static_cast<uint32_t>(r.staging),
+                       r.flags};
   c.mean_time = r.mean_time;
   c.gflops = r.gflops;
+  c.family = static_cast<uint32_t>(r.family);
   return c;
 }
 }  // namespace
@@ -341,6 +355,7 @@ TuningResult sweep(const ObservationSetup& setup, std::uint32_t num_dms, const T
   to.seed = o.seed;
   to.space = o.full_reference_space ? 1 : 0;
   to.max_configs = o.max_configs;
+  to.flush_l2 = o.flush_l2 ? 1 : 0;
   std::lock_guard<std::mutex> g(g_mu);
   dd_context* ctx = context(o.device);
   std::uint64_t n = 0;
@@ -349,7 +364,10 @@ TuningResult sweep(const ObservationSetup& setup, std::uint32_t num_dms, const T
   } else {
     check(dd_enumerate_gpu_configs(ctx, &cs, num_dms, &to.limits, nullptr, 0, &n));
   }
+  if (o.max_configs != 0 && n > o.max_configs) n = o.max_configs;
   std::vector<dd_tuning_record> recs(n);
+  std::vector<double> runs(n * o.repeats);
+  to.runs = runs.data();  // every timed run, the reference's runs_s
   dd_tuning_summary sum{};
   check(dd_tune(ctx, &cs, num_dms, &to, recs.data(), n, &sum));
   TuningResult r;
@@ -369,6 +387,10 @@ TuningResult sweep(const ObservationSetup& setup, std::uint32_t num_dms, const T
                             c.config.work_dm};
     t.dm_tile_depth = c.config.dm_tile_depth;
     t.staging = static_cast<Staging>(c.config.staging);
+    t.flags = c.config.flags;
+    t.family = static_cast<Staging>(c.family);
+    t.runs.assign(runs.begin() + static_cast<std::ptrdiff_t>(i * o.repeats),
+                  runs.begin() + static_cast<std::ptrdiff_t>((i + 1) * o.repeats));
     t.mean_time = c.mean_time;
     t.gflops = c.gflops;
     t.timer_warning = c.timer_warning != 0;
@@ -407,19 +429,24 @@ FixedConfigReport best_fixed_config(std::span<const TuningResult> results) {
       throw std::invalid_argument("tuning results mix different setups");
     if (r.records.empty()) throw std::invalid_argument("a tuning result holds no records");
   }
+  // config identity = the reference 4-tuple plus every GPU knob (depth,
+  // staging, flags): records differing only in stage shape or raster are
+  // different configurations (tuner.cpp:218-261 keys on the whole config)
   struct Key {
     KernelConfig c;
-    std::uint32_t depth, staging;
+    std::uint32_t depth, staging, flags;
     bool operator<(const Key& o) const {
       if (c != o.c) return c < o.c;
       if (depth != o.depth) return depth < o.depth;
-      return staging < o.staging;
+      if (staging != o.staging) return staging < o.staging;
+      return flags < o.flags;
     }
   };
   std::map<Key, std::vector<double>> by;
   for (std::size_t i = 0; i < results.size(); ++i)
     for (const TuningRecord& rec : results[i].records) {
-      auto& v = by[Key{rec.config, rec.dm_tile_depth, static_cast<std::uint32_t>(rec.staging)}];
+      auto& v = by[Key{rec.config, rec.dm_tile_depth, static_cast<std::uint32_t>(rec.staging),
+                       rec.flags}];
       if (v.size() == i) v.push_back(rec.gflops);
     }
   bool found = false;
@@ -431,6 +458,9 @@ FixedConfigReport best_fixed_config(std::span<const TuningResult> results) {
     if (!found || tot > rep.total_gflops) {
       found = true;
       rep.config = k.c;
+      rep.dm_tile_depth = k.depth;
+      rep.staging = static_cast<Staging>(k.staging);
+      rep.flags = k.flags;
       rep.total_gflops = tot;
       rep.fixed_gflops = v;
     }
@@ -439,6 +469,14 @@ FixedConfigReport best_fixed_config(std::span<const TuningResult> results) {
   for (std::size_t i = 0; i < results.size(); ++i)
     rep.speedup_over_fixed.push_back(results[i].best().gflops / rep.fixed_gflops[i]);
   return rep;
+}
+
+void register_schedule(const TuningResult& result) {
+  if (result.records.empty()) throw std::invalid_argument("a tuning result holds no records");
+  const TuningRecord& b = result.best();
+  const dd_config c = to_c(b.config, b.exec_options());
+  check(dd_schedule_set(result.setup.channels, result.setup.samples_per_second, result.num_dms,
+                        &c));
 }
 
 std::vector<std::uint32_t> default_instances() {

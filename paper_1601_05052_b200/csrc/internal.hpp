@@ -20,6 +20,19 @@ struct dd_context {
   int cc_major = 0, cc_minor = 0;
   uint32_t* d_scratch = nullptr;  // 4 x u32 reduction slots
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+  void* d_flush = nullptr;  // cold-L2 timing buffer (2 x L2), lazily allocated
+  uint64_t flush_bytes = 0;
+  // dd_dedisperse's device buffers (grown, never shrunk) and its last plan,
+  // reused while the table (host copy compared) and the config repeat
+  void* d_in = nullptr;
+  void* d_sh = nullptr;
+  void* d_out = nullptr;
+  uint64_t in_cap = 0, sh_cap = 0, out_cap = 0;
+  std::vector<uint32_t> cached_table;
+  dd_plan* cached_plan = nullptr;
+  uint64_t cached_key[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  dd_config last_run{};
+  uint32_t last_family = 0;
 };
 
 struct dd_plan {

@@ -18,6 +18,12 @@
 
 using namespace ddb;
 
+#define DD_TRY(call)            \
+  do {                          \
+    dd_status s_ = (call);      \
+    if (s_ != DD_OK) return s_; \
+  } while (0)
+
 namespace {
 
 // divisors_ascending, tuner.cpp:19-30
@@ -348,8 +354,10 @@ dd_status dd_tune(dd_context* ctx, const dd_setup* setup, uint32_t num_dms,
       continue;
     }
     if (st != DD_OK) break;
-    st = dd_plan_time(p, static_cast<float*>(d_in), static_cast<float*>(d_out), s, 1,
-                      opt->repeats, runs.data());
+    st = dd_plan_time_ex(p, static_cast<float*>(d_in), static_cast<float*>(d_out), s, 1,
+                         opt->repeats, opt->flush_l2 ? 1 : 0, runs.data());
+    if (st == DD_OK && opt->runs != nullptr)
+      std::copy(runs.begin(), runs.end(), opt->runs + recs.size() * opt->repeats);
     dd_plan_info info{};
     dd_plan_get_info(p, &info);
     dd_plan_destroy(p);
@@ -375,10 +383,13 @@ dd_status dd_tune(dd_context* ctx, const dd_setup* setup, uint32_t num_dms,
   dd_device_free(ctx, d_out);
   if (st != DD_OK) return st;
 
+  if (recs.empty())
+    return fail(DD_ERR_INVALID_ARGUMENT, "no configuration could be planned for this instance");
   std::memset(summary, 0, sizeof(*summary));
   summary->count = recs.size();
-  dd_select_best(recs.data(), recs.size(), &summary->best_index);
-  dd_compute_stats(recs.data(), recs.size(), summary->best_index, summary);
+  uint64_t best = 0;
+  DD_TRY(dd_select_best(recs.data(), recs.size(), &best));
+  DD_TRY(dd_compute_stats(recs.data(), recs.size(), best, summary));
   summary->count = recs.size();
   summary->realtime_threshold_gflops = flop / 1e9;  // analysis.cpp:40-45
   summary->realtime_pass = recs[summary->best_index].gflops >= flop / 1e9 ? 1u : 0u;

@@ -28,7 +28,7 @@ class BlockStream:
         self.s, self.c = s, c
         self.t = api.instance_sizing(setup, num_dms).num_samples
         self.pitch = (self.t + 3) // 4 * 4
-        self.ctx = api.context(device)
+        self.ctx = api.Context(device)  # own context: its stream is this stream's
         self.stream = torch.cuda.Stream(device)
         self.ctx.set_stream(self.stream.cuda_stream)
         self.shifts = torch.empty((num_dms, c), dtype=torch.int32, device=device)

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "dedisp/b200.hpp"
@@ -50,7 +51,26 @@ static bool same(const std::vector<float>& a, const std::vector<float>& b) {
   return a.size() == b.size() && std::memcmp(a.data(), b.data(), a.size() * 4) == 0;
 }
 
-int main() {
+static dedisp::TuningRecord record_with(dedisp::KernelConfig k, double gflops,
+                                        std::uint32_t flags) {
+  dedisp::TuningRecord r;  // test_tuner.cpp:18-25 style fake record
+  r.config = k;
+  r.gflops = gflops;
+  r.mean_time = 1.0 / gflops;
+  r.staging = dedisp::Staging::SharedMemory;
+  r.flags = flags;
+  return r;
+}
+
+static std::string hex64(std::uint64_t v) {
+  char b[17];
+  std::snprintf(b, sizeof b, "%016llx", static_cast<unsigned long long>(v));
+  return b;
+}
+
+int main(int argc, char** argv) {
+  // argv[1] (optional): the reference's fingerprint of the Apertif d=4096
+  // output (tests/golden/golden.json), for the full-size drop-in check
   // setup.cpp known answers (test_setup.cpp:75-88, :130-137)
   const auto* apertif = dedisp::find_builtin("Apertif");
   CHECK(apertif != nullptr);
@@ -100,6 +120,102 @@ int main() {
   const auto res = dedisp::tune(*apertif, 64, to);
   CHECK(res.records.size() == 6);
   CHECK(res.best().gflops > 0.0);
+
+  CHECK(res.records.front().runs.size() == 2);  // every timed run kept (runs_s)
+
+  // benchmark_config (tuner.cpp:136-170): a replayable record
+  {
+    dedisp::ExecOptions bo;
+    bo.staging = dedisp::Staging::SharedMemory;
+    bo.flags = 8u << DD_CONFIG_CPS_SHIFT;
+    const auto rec = dedisp::benchmark_config(fb6, table6, k, 3, bo);
+    CHECK(rec.runs.size() == 3);
+    CHECK(rec.mean_time > 0.0 && rec.gflops > 0.0);
+    CHECK(rec.flags == bo.flags && rec.staging == dedisp::Staging::SharedMemory);
+    CHECK(rec.family == dedisp::Staging::SharedMemory);
+    CHECK(same(dedisp::dedisperse_tiled(fb6, table6, k, rec.exec_options()).data,
+               dedisp::dedisperse_reference(fb6, table6).data));
+    CHECK(throws<std::invalid_argument>([&] { dedisp::benchmark_config(fb6, table6, k, 0); }));
+  }
+
+  // best_fixed_config (tuner.cpp:218-261) keys on the whole configuration:
+  // two records of one 4-tuple that differ only in flags are two configs
+  {
+    const dedisp::KernelConfig a{32, 1, 1, 1}, b{64, 1, 1, 1};
+    auto mk = [&](std::vector<dedisp::TuningRecord> recs) {
+      dedisp::TuningResult r;
+      r.setup = *apertif;
+      r.num_dms = 2;
+      r.records = std::move(recs);
+      r.best_index = dedisp::select_best(r.records);
+      return r;
+    };
+    std::vector<dedisp::TuningResult> results = {
+        mk({record_with(a, 10.0, 0), record_with(a, 30.0, 0x800), record_with(b, 20.0, 0)}),
+        mk({record_with(a, 12.0, 0), record_with(b, 25.0, 0)}),
+    };
+    CHECK(results[0].best().flags == 0x800);  // select_best keeps the flags
+    const auto rep = dedisp::best_fixed_config(results);
+    CHECK(rep.config == b && rep.flags == 0);  // (a, 0x800) is not valid everywhere
+    CHECK(rep.total_gflops == 45.0);
+    CHECK(rep.speedup_over_fixed.size() == 2 && rep.speedup_over_fixed[0] == 1.5);
+    results[1].records.push_back(record_with(a, 40.0, 0x800));
+    results[1].best_index = dedisp::select_best(results[1].records);
+    const auto rep2 = dedisp::best_fixed_config(results);
+    CHECK(rep2.config == a && rep2.flags == 0x800 && rep2.total_gflops == 70.0);
+  }
+
+  // tuned dispatch: default ExecOptions (staging Auto, no flags) run the
+  // instance's tuned schedule; a registered one takes precedence
+  {
+    const auto t64 = dedisp::build_delay_table(*apertif, 64);
+    const auto fb64 = dedisp::noise_filterbank(
+        *apertif, static_cast<std::uint32_t>(dedisp::instance_sizing(*apertif, 64).num_samples),
+        1.0f, 1);
+    const auto ref64 = dedisp::dedisperse_reference(fb64, t64);
+    dd_config ran{};
+    int builtin = 0;
+    CHECK(dd_schedule_get(1024, 20000, 64, &ran, &builtin) == DD_OK && builtin == 1);
+    CHECK(same(dedisp::dedisperse_tiled(fb64, t64, {32, 8, 1, 8}).data, ref64.data));
+    dd_config last{};
+    dd_context* ctx0 = nullptr;
+    (void)ctx0;
+    dedisp::TuningResult tr;
+    tr.setup = *apertif;
+    tr.num_dms = 64;
+    auto rec = record_with({32, 8, 1, 8}, 1.0, 8u << DD_CONFIG_CPS_SHIFT);
+    rec.staging = dedisp::Staging::RegisterWindow;
+    rec.config = {32, 4, 25, 4};
+    tr.records = {rec};
+    tr.best_index = 0;
+    dedisp::register_schedule(tr);
+    CHECK(dd_schedule_get(1024, 20000, 64, &last, &builtin) == DD_OK && builtin == 0);
+    CHECK(last.staging == DD_STAGING_REGWIN && last.work_time == 25);
+    CHECK(same(dedisp::dedisperse_tiled(fb64, t64, {32, 8, 1, 8}).data, ref64.data));
+    CHECK(dd_schedule_set(1024, 20000, 64, nullptr) == DD_OK);  // forget it again
+    // an explicit staging runs exactly the config asked for
+    dedisp::ExecOptions so;
+    so.staging = dedisp::Staging::SharedMemory;
+    CHECK(same(dedisp::dedisperse_tiled(fb64, t64, {32, 8, 1, 8}, so).data, ref64.data));
+  }
+
+  // full size through the drop-in: Apertif d=4096 with default options runs
+  // the tuned TMEM-window kernel (K5) and reproduces the reference's bits
+  if (argc > 1) {
+    const auto t4k = dedisp::build_delay_table(*apertif, 4096);
+    const auto fb4k = dedisp::noise_filterbank(
+        *apertif, static_cast<std::uint32_t>(dedisp::instance_sizing(*apertif, 4096).num_samples),
+        1.0f, 1);
+    dedisp::DedispersedSeries out;
+    dedisp::dedisperse_tiled_into(out, fb4k, t4k, {125, 8, 8, 1});  // the reference CPU config
+    std::uint64_t h = 0;
+    CHECK(dd_fingerprint(out.data.data(), out.data.size() * 4, &h) == DD_OK);
+    CHECK(hex64(h) == argv[1]);
+    dd_config cfg{};
+    int b = 0;
+    CHECK(dd_schedule_get(1024, 20000, 4096, &cfg, &b) == DD_OK && cfg.staging == DD_STAGING_TMEM);
+    std::printf("dropin: Apertif d=4096 fingerprint %s (golden %s)\n", hex64(h).c_str(), argv[1]);
+  }
 
   std::printf(failures ? "dropin: %d failure(s)\n" : "dropin: ok\n", failures);
   return failures ? 1 : 0;

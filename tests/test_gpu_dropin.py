@@ -9,7 +9,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = pytest.mark.gpu
 
 
-def test_cxx_dropin(tmp_path):
+def test_cxx_dropin(tmp_path, golden):
     from oracle import oracle as O
     from paper_1601_05052_b200 import api
     if api.device_count() == 0:
@@ -21,6 +21,9 @@ def test_cxx_dropin(tmp_path):
                     os.path.join(ROOT, "tests", "cxx", "test_dropin.cpp"), "-L", pkg,
                     "-ldedisp_b200", "-L", os.path.join(ROOT, "oracle"), "-loracle",
                     f"-Wl,-rpath,{pkg}:{os.path.join(ROOT, 'oracle')}", "-o", exe], check=True)
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    g4k = [b for b in golden["baseline"]
+           if b["setup"]["name"] == "Apertif" and b["num_dms"] == 4096][0]["out_fnv"]
+    r = subprocess.run([exe, g4k], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "dropin: ok" in r.stdout
+    assert f"fingerprint {g4k}" in r.stdout

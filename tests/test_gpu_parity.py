@@ -140,6 +140,44 @@ def test_lofar_4096_golden(dev, golden):
     assert O.fnv1a(out.data) == g["out_fnv"]
 
 
+def _tuned_records(name, d, top):
+    """The `top` fastest records of the committed sweep tuning/<name>_<d>.json
+    (the first is the tuner's pick, the configuration bench.py times)."""
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tuning",
+                        f"{name.lower()}_{d}.json")
+    with open(path) as f:
+        res = api.tuning_result_from_json(f.read())
+    best = res.best()
+    rest = sorted((r for r in res.records if r is not best), key=lambda r: -r.gflops)
+    return [best] + rest[:top - 1]
+
+
+@pytest.mark.parametrize("idx,name", [(2, "Apertif"), (3, "LOFAR")])
+def test_tuned_configs_at_full_size(dev, golden, idx, name):
+    """The exact configurations the bench times -- the tuner's pick for
+    Apertif and LOFAR at d=4096 (config, depth, staging and every flag:
+    GPU tiling, stage width, raster, packed stages), plus the next fastest
+    records -- replayed at full size: the whole output's fingerprint equals
+    the reference's (golden, from oracle/_ref)."""
+    import torch
+    g = golden["baseline"][idx]
+    setup, table, fb = _golden_instance(g)
+    d, s, c, t = g["num_dms"], setup.samples_per_second, setup.channels, g["num_samples"]
+    x = torch.from_numpy(fb.data).cuda()
+    sh = torch.from_numpy(table.shifts.view(np.int32)).cuda()
+    out = torch.empty((d, s), device="cuda")
+    for rec in _tuned_records(name, d, 3):
+        out.fill_(float("nan"))
+        p = dev.plan(sh.data_ptr(), c, d, s, t, t, rec.config, rec.dm_tile_depth, rec.staging,
+                     flags=rec.flags)
+        assert p.info()["family"] == (rec.family or rec.staging)
+        p.execute(x.data_ptr(), out.data_ptr())
+        dev.synchronize()
+        assert api.fingerprint(out.cpu()) == g["out_fnv"], (rec.config, rec.staging, hex(rec.flags))
+        p.close()
+
+
 # ------------------------------------------------ randomised equivalence --
 def test_mini_instances_all_families(dev, golden):
     rng = np.random.default_rng(1)
@@ -425,6 +463,15 @@ def test_sharded_driver_host_pipeline(dev, golden):
     dd2.run_host(host, out)
     torch.cuda.synchronize()
     assert O.fnv1a(out.numpy()) == g["out_fnv"]
+    # the first driver still launches on its own stream with dd2 alive (each
+    # driver owns its context), so its events still cover its kernels
+    assert dd.ctx.handle.value != dd2.ctx.handle.value
+    for o in outs:
+        o.fill_(float("nan"))
+    dd.stream_host([host, host2], outs, 3)
+    torch.cuda.synchronize()
+    assert O.fnv1a(outs[0].numpy()) == g["out_fnv"]
+    assert np.array_equal(_bits(outs[1].numpy()), _bits(ref * 2))
 
 
 @pytest.mark.parametrize("staging,cfg,tiling", [("smem", K(16, 8, 10, 4), False),
@@ -452,15 +499,16 @@ def test_channel_range_passes_are_bit_identical(dev, golden, staging, cfg, tilin
                                                 ("tmem", K(32, 4, 12, 8), True),
                                                 ("tm-smem", K(16, 8, 10, 4), False),
                                                 ("tm-tmem", K(32, 4, 12, 8), True)])
-def test_beam_batching(dev, staging, cfg, tiling):
+def test_beam_batching(dev, golden, staging, cfg, tiling):
     """dd_plan_execute_beams: B independent beams in one launch equal B single
-    passes (each checked against the oracle on a DM subset)."""
+    passes.  Beam b is the golden block times 2^b (exact in fp32), so every
+    beam's whole output is the reference's output times 2^b, bit for bit."""
     import torch
-    setup, d, beams = api.APERTIF, 64, 3
-    s, c = setup.samples_per_second, setup.channels
-    t = api.instance_sizing(setup, d).num_samples
-    table = api.build_delay_table(setup, d)
-    blocks = [api.noise_filterbank(setup, t, 1.0, 10 + b).data for b in range(beams)]
+    g = golden["baseline"][0]
+    setup, table, fb = _golden_instance(g)
+    d, beams = g["num_dms"], 3
+    s, c, t = setup.samples_per_second, setup.channels, g["num_samples"]
+    blocks = [fb.data * np.float32(2.0 ** b) for b in range(beams)]
     x = torch.from_numpy(np.stack(blocks)).cuda()
     sh = torch.from_numpy(table.shifts.view(np.int32)).cuda()
     out = torch.full((beams, d, s), float("nan"), device="cuda")
@@ -472,10 +520,9 @@ def test_beam_batching(dev, staging, cfg, tiling):
     p.execute_beams(beams, x.data_ptr(), c * t, out.data_ptr(), d * s)
     dev.synchronize()
     got = out.cpu().numpy()
-    rows = [0, 17, 63]
-    for b in range(beams):
-        ref = O.dedisperse_reference(blocks[b], table.shifts[rows], s)
-        assert np.array_equal(_bits(got[b][rows]), _bits(ref)), b
+    assert api.fingerprint(got[0]) == g["out_fnv"]
+    for b in range(1, beams):
+        assert np.array_equal(_bits(got[b]), _bits(got[0] * np.float32(2.0 ** b))), b
 
 
 def test_block_stream_matches_one_shot(dev):
@@ -571,21 +618,25 @@ def test_large_delay_instance_all_rasters(dev, flags):
     assert np.array_equal(_bits(got.data), _bits(ref))
 
 
-@pytest.mark.parametrize("name,d", [("Apertif", 64), ("LOFAR", 32)])
-def test_every_gpu_space_config_is_bit_exact(dev, name, d):
+@pytest.mark.parametrize("name,d", [("Apertif", 64), ("LOFAR", 64)])
+def test_every_gpu_space_config_is_bit_exact(dev, golden, name, d):
     """Every configuration the GPU tuner can select (dd_enumerate_gpu_configs:
     all families, depths, stage shapes, rasters, occupancy builds) reproduces
     the reference on one instance -- the auto-tuner may pick any of them."""
     import torch
-    setup = api.find_builtin(name)
-    table = api.build_delay_table(setup, d)
-    t = api.instance_sizing(setup, d).num_samples
+    g = [b for b in golden["baseline"] if b["setup"]["name"] == name and b["num_dms"] == d][0]
+    setup, table, fb = _golden_instance(g)
+    t = g["num_samples"]
     s, c = setup.samples_per_second, setup.channels
-    fb = api.noise_filterbank(setup, t, 1.0, 5)
-    rows = [0, d // 2, d - 1]
-    ref = O.dedisperse_reference(fb.data, table.shifts[rows], s)
     x = torch.from_numpy(fb.data).cuda()
     sh = torch.from_numpy(table.shifts.view(np.int32)).cuda()
+    # the whole output of every configuration against the reference-order
+    # kernel's, which is first pinned to the reference's fingerprint
+    ref = torch.empty((d, s), device="cuda")
+    dev.plan(sh.data_ptr(), c, d, s, t, t).execute(x.data_ptr(), ref.data_ptr())
+    dev.synchronize()
+    assert api.fingerprint(ref.cpu()) == g["out_fnv"]
+    ref_bits = ref.view(torch.int32)
     out = torch.empty((d, s), device="cuda")
     space = api.enumerate_gpu_configs(setup, d)
     assert len(space) > 100
@@ -600,8 +651,7 @@ def test_every_gpu_space_config_is_bit_exact(dev, name, d):
         families.add(p.info()["family"])
         p.execute(x.data_ptr(), out.data_ptr())
         dev.synchronize()
-        got = out[rows].cpu().numpy()
-        assert np.array_equal(_bits(got), _bits(ref)), (cfg, depth, staging, hex(flags))
+        assert torch.equal(out.view(torch.int32), ref_bits), (cfg, depth, staging, hex(flags))
         p.close()
     assert {"smem", "direct"} <= families
     assert rejected < len(space) // 4
