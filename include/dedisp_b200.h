@@ -321,6 +321,14 @@ dd_status dd_schedule_get(uint32_t channels, uint32_t samples_per_second, uint32
  * context actually ran (the tuned one, or the caller's config). */
 dd_status dd_last_run_config(dd_context* ctx, dd_config* cfg, uint32_t* family);
 
+/* ------------------------------------------------- checked builds ---- */
+/* Device bounds violations counted by a checked build of this library
+ * (libdedisp_b200_checked.so, -DDDB_CHECKED: every staged window read, bulk
+ * copy and output store bounds-checked on the device) on the current
+ * device since the last reset; *checked = 0 and count 0 in release builds.
+ * Synchronises the device. */
+dd_status dd_debug_violations(uint64_t* count, int* checked, int reset);
+
 /* ------------------------------------------------------ fingerprints -- */
 /* FNV-1a 64 (basis 0xcbf29ce484222325, prime 0x100000001b3) over `bytes`
  * bytes of host memory: the fingerprint the golden fixtures use

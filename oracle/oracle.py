@@ -147,6 +147,12 @@ def ref_lib():
             L.ref_job_output.restype = f32p
             L.ref_job_output.argtypes = [C.c_void_p]
             L.ref_job_destroy.argtypes = [C.c_void_p]
+            L.ref_parse_sigproc.argtypes = [C.c_char_p, C.c_uint64, u32p, u64p, f32p, u64p,
+                                            C.POINTER(C.c_double), C.POINTER(C.c_double), u32p]
+            if hasattr(L, "ref_tuning_roundtrip"):
+                L.ref_tuning_roundtrip.argtypes = [C.c_char_p, u32p, u64p, u32p,
+                                                   C.POINTER(C.c_double), u32p, C.c_char_p,
+                                                   C.c_uint64, u64p]
             _REF = L
     return _REF
 
@@ -246,3 +252,60 @@ def enumerate_configs(num_dms: int, s: int, max_block_items=1024, max_accumulato
     buf = (ConfigC * max(n, 1))()
     L.or_enumerate_configs(num_dms, s, max_block_items, max_accumulators, buf, n)
     return [(b.items_time, b.items_dm, b.work_time, b.work_dm) for b in buf[:n]]
+
+
+# ------------------------------------------- reference I/O (oracle/_ref) --
+def sigproc_bytes(data: np.ndarray, rate: int, fch1: float, foff: float) -> bytes:
+    """A SIGPROC stream in the reference's subset (sigproc.cpp:201-250 writes
+    the same layout): length-prefixed keywords, little-endian values, payload
+    float32 time-major [samples][channels] with channel 0 the highest."""
+    import struct
+    kw = lambda k: struct.pack("<I", len(k)) + k.encode()
+    t, c = data.shape
+    head = (kw("HEADER_START") + kw("nchans") + struct.pack("<i", c) + kw("tsamp") +
+            struct.pack("<d", 1.0 / rate) + kw("fch1") + struct.pack("<d", fch1) + kw("foff") +
+            struct.pack("<d", foff) + kw("nbits") + struct.pack("<i", 32) + kw("nifs") +
+            struct.pack("<i", 1) + kw("HEADER_END"))
+    return head + np.ascontiguousarray(data, np.float32).tobytes()
+
+
+def ref_parse_sigproc(stream: bytes):
+    """The reference's parse_sigproc (sigproc.cpp:83-191) on a byte stream:
+    (channel-major data lowest first, (f_min, channel_width, rate)) or, on
+    format_error, (None, byte_offset)."""
+    R = ref_lib()
+    if R is None:
+        raise RuntimeError("oracle/_ref is not built")
+    ch, ns, bad = C.c_uint32(), C.c_uint64(), C.c_uint64()
+    fm, cw, rate = C.c_double(), C.c_double(), C.c_uint32()
+    st = R.ref_parse_sigproc(stream, len(stream), C.byref(ch), C.byref(ns), None, C.byref(bad),
+                             C.byref(fm), C.byref(cw), C.byref(rate))
+    if st == 4:
+        return None, bad.value
+    assert st == 0, st
+    out = np.empty((ch.value, ns.value), np.float32)
+    assert R.ref_parse_sigproc(stream, len(stream), C.byref(ch), C.byref(ns), _p(out, C.c_float),
+                               C.byref(bad), C.byref(fm), C.byref(cw), C.byref(rate)) == 0
+    return out, (fm.value, cw.value, rate.value)
+
+
+def ref_tuning_roundtrip(text: str):
+    """The reference's tuning_result_from_json then tuning_result_to_json
+    (report_io.cpp:58-157): a summary of what it read and its own document,
+    or None when oracle/_ref was built without a json.hpp."""
+    R = ref_lib()
+    if R is None or not hasattr(R, "ref_tuning_roundtrip"):
+        return None
+    n, best, dms, need = C.c_uint32(), C.c_uint64(), C.c_uint32(), C.c_uint64()
+    cfg, g = (C.c_uint32 * 4)(), C.c_double()
+    enc = text.encode()
+    st = R.ref_tuning_roundtrip(enc, C.byref(n), C.byref(best), cfg, C.byref(g), C.byref(dms),
+                                None, 0, C.byref(need))
+    if st == 4:
+        raise ValueError("reference rejected the document (format_error)")
+    assert st == 0, st
+    buf = C.create_string_buffer(need.value + 1)
+    R.ref_tuning_roundtrip(enc, C.byref(n), C.byref(best), cfg, C.byref(g), C.byref(dms), buf,
+                           need.value + 1, C.byref(need))
+    return {"records": n.value, "best_index": best.value, "best_config": tuple(cfg),
+            "best_gflops": g.value, "num_dms": dms.value, "json": buf.value.decode()}

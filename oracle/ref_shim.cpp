@@ -13,7 +13,11 @@
 //   dedisperse_tiled_into                       kernels.hpp:102-104
 //   count_loads                                 kernels.hpp:114-115
 //   enumerate_configs                           tuner.hpp:61-63
+//   parse_sigproc                               filterbank.hpp:69 (sigproc.cpp:83-191)
+//   tuning_result_from_json / _to_json          report_io.hpp:11-14 (report_io.cpp:58-157)
 #include <cstdint>
+#include <span>
+#include <string>
 #include <cstring>
 #include <exception>
 #include <stdexcept>
@@ -25,6 +29,9 @@
 #include "dedisp/setup.hpp"
 #include "dedisp/thread_pool.hpp"
 #include "dedisp/tuner.hpp"
+#ifdef REF_HAVE_JSON
+#include "dedisp/report_io.hpp"
+#endif
 
 namespace {
 
@@ -217,5 +224,64 @@ std::int64_t ref_enumerate_configs(std::uint32_t num_dms, std::uint32_t s,
     return -1;
   }
 }
+
+// parse_sigproc over an in-memory stream.  Returns 0 and the parsed
+// channel-major data (lowest channel first) when `out` holds channels x
+// samples floats (call once with out = NULL for the sizes); 4 on a
+// format_error, whose byte offset lands in *bad_offset.
+int ref_parse_sigproc(const std::uint8_t* bytes, std::uint64_t n, std::uint32_t* channels,
+                      std::uint64_t* samples, float* out, std::uint64_t* bad_offset,
+                      double* f_min, double* channel_width, std::uint32_t* rate) {
+  try {
+    const dedisp::Filterbank fb = dedisp::parse_sigproc(std::span<const std::uint8_t>(bytes, n));
+    *channels = fb.setup.channels;
+    *samples = fb.num_samples;
+    *f_min = fb.setup.f_min;
+    *channel_width = fb.setup.channel_width;
+    *rate = fb.setup.samples_per_second;
+    if (out != nullptr) std::memcpy(out, fb.data.data(), fb.data.size() * sizeof(float));
+    return 0;
+  } catch (const dedisp::format_error& e) {
+    *bad_offset = e.byte_offset();
+    return 4;
+  } catch (...) {
+    return 3;
+  }
+}
+
+#ifdef REF_HAVE_JSON
+// tuning_result_from_json, then a summary of what the reference read and
+// its own re-serialisation (tuning_result_to_json) into `json_out`
+// (capacity cap; *json_len = the needed size).  Returns 4 on format_error.
+int ref_tuning_roundtrip(const char* text, std::uint32_t* num_records, std::uint64_t* best_index,
+                         std::uint32_t* best_config, double* best_gflops,
+                         std::uint32_t* num_dms, char* json_out, std::uint64_t cap,
+                         std::uint64_t* json_len) {
+  try {
+    const dedisp::TuningResult r = dedisp::tuning_result_from_json(text);
+    *num_records = static_cast<std::uint32_t>(r.records.size());
+    *best_index = r.best_index;
+    const dedisp::TuningRecord& b = r.best();
+    best_config[0] = b.config.items_time;
+    best_config[1] = b.config.items_dm;
+    best_config[2] = b.config.work_time;
+    best_config[3] = b.config.work_dm;
+    *best_gflops = b.gflops;
+    *num_dms = r.num_dms;
+    const std::string j = dedisp::tuning_result_to_json(r);
+    *json_len = j.size();
+    if (json_out != nullptr && cap > 0) {
+      const std::size_t k = j.size() < cap - 1 ? j.size() : static_cast<std::size_t>(cap - 1);
+      std::memcpy(json_out, j.data(), k);
+      json_out[k] = 0;
+    }
+    return 0;
+  } catch (const dedisp::format_error&) {
+    return 4;
+  } catch (...) {
+    return 3;
+  }
+}
+#endif
 
 }  // extern "C"

@@ -128,6 +128,7 @@ SIGNATURES = {
     "dd_plan_time": (i32, [P, P, P, u64, u32, u32, pdbl]),
     "dd_plan_time_ex": (i32, [P, P, P, u64, u32, u32, C.c_int, pdbl]),
     "dd_fingerprint": (i32, [P, u64, pu64]),
+    "dd_debug_violations": (i32, [pu64, C.POINTER(C.c_int), C.c_int]),
     "dd_schedule_set": (i32, [u32, u32, u32, C.POINTER(dd_config)]),
     "dd_schedule_get": (i32, [u32, u32, u32, C.POINTER(dd_config), C.POINTER(C.c_int)]),
     "dd_last_run_config": (i32, [P, C.POINTER(dd_config), pu32]),

@@ -19,6 +19,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdedisp_b200.so")
+LIB_CHECKED = os.path.join(PKG, "libdedisp_b200_checked.so")
 SOURCES = ["table.cu", "dedisp.cu", "abi.cu", "tuner.cu", "ingest.cu", "host.cpp"]
 HEADERS = ["common.cuh", "internal.hpp", "regwin_dispatch.cuh", "schedules.inc"]
 PUBLIC = [os.path.join(ROOT, "include", "dedisp_b200.h"),
@@ -52,9 +53,15 @@ def gen_dispatch() -> None:
             f.write(r.stdout)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """checked=True: libdedisp_b200_checked.so, the same library with every
+    staged shared-memory read, bulk copy and output store bounds-checked on
+    the device (-DDDB_CHECKED; dd_debug_violations) -- the memcheck stand-in
+    (tests/test_gpu_checked.py)."""
     gen_dispatch()
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build_checked" if checked else "build")
+    lib = LIB_CHECKED if checked else LIB
+    extra = ["-DDDB_CHECKED"] if checked else []
     os.makedirs(objdir, exist_ok=True)
     deps_common = [os.path.join(CSRC, h) for h in HEADERS] + PUBLIC + [__file__]
     objs = []
@@ -64,7 +71,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
         if force or _stale(obj, [path] + deps_common):
             if src.endswith(".cu"):
-                cmd = [nvcc()] + ARCH + FLAGS + ["-c", path, "-o", obj]
+                cmd = [nvcc()] + ARCH + FLAGS + extra + ["-c", path, "-o", obj]
             else:  # host-only C++ (the C++20 drop-in API and the tuner)
                 cmd = [nvcc(), "-x", "c++", "-O3", "-std=c++20", "-Xcompiler", "-fPIC,-O3,-Wall",
                        "-I" + os.path.join(ROOT, "include"), "-c", path, "-o", obj]
@@ -76,14 +83,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 sys.stderr.write(r.stderr)
             with open(obj + ".ptxas.txt", "w") as f:
                 f.write(r.stderr)
-    if force or _stale(LIB, objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lpthread"]
+    if force or _stale(lib, objs):
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", lib] + objs + ["-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("nvcc link failed")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                checked="--checked" in sys.argv))

@@ -1115,6 +1115,17 @@ dd_status dd_dedisperse_device(dd_context* c, const float* d_in, uint32_t channe
   return st;
 }
 
+dd_status dd_debug_violations(uint64_t* count, int* checked, int reset) {
+  if (count == nullptr) return fail(DD_ERR_INVALID_ARGUMENT, "count is null");
+  unsigned long long n = 0;
+  int chk = 0;
+  DD_CUDA(cudaDeviceSynchronize());
+  DD_CUDA(debug_violations(&n, &chk, reset));
+  *count = n;
+  if (checked) *checked = chk;
+  return DD_OK;
+}
+
 dd_status dd_fingerprint(const void* data, uint64_t bytes, uint64_t* out) {
   if (out == nullptr || (data == nullptr && bytes != 0))
     return fail(DD_ERR_INVALID_ARGUMENT, "null argument");

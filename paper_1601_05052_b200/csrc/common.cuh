@@ -8,6 +8,25 @@
 
 namespace ddb {
 
+// ------------------------------------------------------- checked builds --
+// DDB_CHECKED (build.py build(checked=True) -> libdedisp_b200_checked.so):
+// every shared-memory window read, bulk-copy source/destination and output
+// store of the staged kernels is bounds-checked on the device and a
+// violation counted (dd_debug_violations).  The pool's GPUs do not allow
+// compute-sanitizer, so this is the memcheck of the hot path
+// (tools/sanitize_cases.py, tests/test_gpu_checked.py).
+#ifdef DDB_CHECKED
+// one counter per translation unit; the staged kernels and its reader
+// (debug_violations) live in dedisp.cu
+static __device__ unsigned long long g_ddb_violations = 0;
+__device__ __forceinline__ void ddb_check(bool ok) {
+  if (!ok) atomicAdd(&g_ddb_violations, 1ull);
+}
+#define DDB_CHECK(cond) ::ddb::ddb_check(static_cast<bool>(cond))
+#else
+#define DDB_CHECK(cond) ((void)0)
+#endif
+
 // ----------------------------------------------------------------- PTX --
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

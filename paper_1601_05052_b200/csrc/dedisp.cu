@@ -7,10 +7,27 @@
 // thread mapping change only the schedule, never that sequence, so every
 // kernel here is bit-identical to dedisperse_reference.  Build flags must
 // not enable fast-math / FTZ (see build.py).
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "common.cuh"
 #include "regwin_dispatch.cuh"
 
 namespace ddb {
+
+// Bounds of the shared-memory stage a consumer is reading (checked builds).
+struct ChkRange {
+#ifdef DDB_CHECKED
+  const float* lo = nullptr;
+  const float* hi = nullptr;
+  __device__ __forceinline__ void check(const float* p, int n) const {
+    DDB_CHECK(p >= lo && p + n <= hi);
+  }
+#else
+  __device__ __forceinline__ void check(const float*, int) const {}
+#endif
+};
 
 // ---------------------------------------------------------------------
 // K2: reference order, one thread per output (dedisperse_reference_into,
@@ -213,6 +230,10 @@ __device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, ui
     const uint32_t end = min((p.t0 + lo + span + a.tile_time + 3u) & ~3u,
                              static_cast<uint32_t>(a.in_pitch));
     const uint32_t bytes = (end - start) * 4u;
+    // the copy stays inside its channel's row and its stage slot
+    DDB_CHECK(start < end && ch0 + cc < a.channels);
+    DDB_CHECK(window_offset<PK>(a, ch0, cc) + (end - start) <=
+              (PK ? a.stage_floats : a.cps * a.win_cap));
     mbar_expect_tx(bar, bytes);
     bulk_g2s(dst + window_offset<PK>(a, ch0, cc), src + static_cast<uint64_t>(cc) * a.in_pitch + start,
              bytes, bar);
@@ -277,6 +298,10 @@ __device__ __forceinline__ void staged_loop_with(const TiledArgs& a, uint8_t* sm
     stage_channels<PK>(a, q, ch0, ncs);
     const uint8_t* rbase = p.recs + slot * a.cps * a.rec_bytes;
     const float* wbase = p.wins + stage_offset<PK>(a, slot);
+#ifdef DDB_CHECKED
+    body.chk.lo = wbase;
+    body.chk.hi = wbase + (PK ? a.stage_floats : a.cps * a.win_cap);
+#endif
     if (active) {
       for (uint32_t cc = 0; cc < ncs; ++cc) {
         const uint32_t* r = reinterpret_cast<const uint32_t*>(rbase + cc * a.rec_bytes);
@@ -313,6 +338,7 @@ struct SmemBody {
   const TiledArgs& a;
   uint32_t it, id;
   float acc[K][W];
+  ChkRange chk;
 
   // IT > 0: items_time fixed at compile time, so a thread's W samples sit
   // at immediate offsets from one address (no per-load address arithmetic)
@@ -335,6 +361,9 @@ struct SmemBody {
     const float* p[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) p[k] = w + r[4 + id + k * a.items_dm];
+#ifdef DDB_CHECKED
+    for (int k = 0; k < K; ++k) chk.check(p[k], (W - 1) * stride() + 1);
+#endif
 #pragma unroll
     for (int n = 0; n + 1 < K * W; n += 2) {
       const int k0 = n / W, j0 = n % W, k1 = (n + 1) / W, j1 = (n + 1) % W;
@@ -358,6 +387,7 @@ struct SmemBody {
   __device__ __forceinline__ void store(uint32_t dm0, uint32_t t0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
+      DDB_CHECK(dm0 + id + k * a.items_dm < a.num_dms);
       float* o =
           beam_out(a) + static_cast<uint64_t>(dm0 + id + k * a.items_dm) * a.out_pitch + t0 + it;
 #pragma unroll
@@ -513,6 +543,7 @@ struct RegWinBody {
   uint32_t col;  // first sample of this lane relative to t0
   uint32_t dml;  // first DM of this warp relative to dm0
   RegWin<K, W, SPAN> rw;
+  ChkRange chk;
 
   __device__ RegWinBody(const TiledArgs& args) : a(args) {
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -532,11 +563,19 @@ struct RegWinBody {
   __device__ __forceinline__ void channel(const uint32_t* r, const float* w) {
     RwChan<K, W, SPAN> c;
     RegWin<K, W, SPAN>::load(c, r, w, col, dml);
+#ifdef DDB_CHECKED
+    if (c.fast) {
+      chk.check(c.base + c.off[0] - c.al, RwGeom<W, SPAN>::kWin);
+    } else {
+      for (int k = 0; k < K; ++k) chk.check(c.base + c.off[k], W);
+    }
+#endif
     rw.compute(c);
   }
   __device__ __forceinline__ void store(uint32_t dm0, uint32_t t0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
+      DDB_CHECK(dm0 + dml + k < a.num_dms);
       float* o = beam_out(a) + static_cast<uint64_t>(dm0 + dml + k) * a.out_pitch + t0 + col;
 #pragma unroll
       for (int j = 0; j < W; ++j)
@@ -649,6 +688,7 @@ struct TmemBody {
   const TiledArgs& a;
   uint32_t col, dml, taddr;
   float acc[K][W];
+  ChkRange chk;
 
   __device__ TmemBody(const TiledArgs& args, uint32_t tmem_base) : a(args) {
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -701,6 +741,11 @@ struct TmemBody {
     n.nv = g.x <= static_cast<uint32_t>((32 + kTail) / 4) ? g.x : 0u;
     n.base = w + col + g.y;  // w: the channel's 16-byte aligned row (kRowBase)
     const float* pa = n.base;
+#ifdef DDB_CHECKED
+    // the unconditional head reads (32 floats, or the predicated ones)
+    chk.check(pa, kFullHead ? 4 * kHeadAlways : 4 * static_cast<int>(min(n.nv, 8u)));
+    if (kFullHead && n.nv > static_cast<uint32_t>(kHeadAlways)) chk.check(pa, 32);
+#endif
     if constexpr (kFullHead) {
       // head vectors unpredicated: columns past the window are never read
       // back, the slot's slack keeps the reads inside shared memory, and
@@ -739,6 +784,9 @@ struct TmemBody {
         // reuse the head's registers once the x32 store has read them
         const float* pa = n.base + 32;
         float* hi = n.win;
+#ifdef DDB_CHECKED
+        chk.check(pa, 4 * static_cast<int>(min(n.nv - 8u, static_cast<uint32_t>(kTail / 4))));
+#endif
         // nv > 8: the first tail vector is always needed
 #pragma unroll
         for (int i = 0; i < kTail / 4; ++i)
@@ -787,6 +835,7 @@ struct TmemBody {
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const float* q = base + static_cast<int32_t>(off[k]);
+        chk.check(q, W);
 #pragma unroll
         for (int j = 0; j < W; ++j) acc[k][j] += q[j];
       }
@@ -815,6 +864,7 @@ struct TmemBody {
   __device__ __forceinline__ void store(uint32_t dm0, uint32_t t0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
+      DDB_CHECK(dm0 + dml + k < a.num_dms);
       float* o = beam_out(a) + static_cast<uint64_t>(dm0 + dml + k) * a.out_pitch + t0 + col;
 #pragma unroll
       for (int j = 0; j < W; ++j)
@@ -1031,9 +1081,39 @@ cudaError_t launch_smem(KernelFn fn, const TiledArgs& a, uint32_t blocks, uint32
   return cudaGetLastError();
 }
 
+cudaError_t debug_violations(unsigned long long* count, int* checked, int reset) {
+#ifdef DDB_CHECKED
+  *checked = 1;
+  cudaError_t e = cudaMemcpyFromSymbol(count, g_ddb_violations, sizeof(*count));
+  if (e == cudaSuccess && reset) {
+    const unsigned long long zero = 0;
+    e = cudaMemcpyToSymbol(g_ddb_violations, &zero, sizeof(zero));
+  }
+  return e;
+#else
+  (void)reset;
+  *checked = 0;
+  *count = 0;
+  return cudaSuccess;
+#endif
+}
+
 cudaError_t prepare_smem(KernelFn fn, uint32_t smem) {
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  // The attribute belongs to the function (per device), not to a plan: it
+  // is only ever raised, so a plan created later with a smaller shared-memory
+  // footprint cannot invalidate the launches of a live plan using the same
+  // kernel with a larger one.
+  static std::mutex mu;
+  static std::map<std::pair<int, KernelFn>, uint32_t> raised;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  uint32_t& cur = raised[{dev, fn}];
+  if (smem <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+  if (e == cudaSuccess) cur = smem;
   // The staged kernels never read through L1 (TMA fills shared memory,
   // outputs are streaming stores): ask for the whole unified array as
   // shared memory so the register budget, not the carveout, sets the

@@ -98,6 +98,8 @@ cudaError_t launch_direct(const TiledArgs& a, uint32_t blocks, uint32_t threads,
 cudaError_t launch_smem(KernelFn fn, const TiledArgs& a, uint32_t blocks, uint32_t threads,
                         uint32_t smem, cudaStream_t st, uint32_t beams = 1);
 cudaError_t prepare_smem(KernelFn fn, uint32_t smem);
+// checked builds (DDB_CHECKED): device bounds violations so far (dedisp.cu)
+cudaError_t debug_violations(unsigned long long* count, int* checked, int reset);
 
 // host logic shared with the tuner (abi.cu)
 dd_limits effective_limits(const dd_limits* l);

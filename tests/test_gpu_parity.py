@@ -550,27 +550,35 @@ def test_block_stream_matches_one_shot(dev):
         assert np.array_equal(_bits(o), _bits(ref)), i
 
 
-def test_sigproc_transpose_on_device(dev):
-    """dd_sigproc_to_filterbank equals the reference's host transpose
-    (sigproc.cpp:177-189: time-major, highest channel first -> channel-major,
-    lowest first) and reports the first non-finite sample."""
+@pytest.mark.parametrize("t,c", [(1001, 37), (40000, 1024), (3, 1), (257, 32)])
+def test_sigproc_transpose_matches_reference(dev, t, c):
+    """dd_sigproc_to_filterbank against the reference's own parse_sigproc
+    (oracle/_ref, sigproc.cpp:83-191) on the same generated stream: the
+    channel-major lowest-first block bit for bit, and the first non-finite
+    sample at the byte offset the reference's format_error reports."""
     import torch
-    rng = np.random.default_rng(4)
-    c, t = 37, 1001
+    if O.ref_lib() is None:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(t + c)
     payload = rng.standard_normal((t, c)).astype(np.float32)
-    expect = payload[:, ::-1].T.copy()
+    stream = O.sigproc_bytes(payload, 20000, 1716.67, -0.29)
+    header_end = len(stream) - payload.nbytes
+    expect, _ = O.ref_parse_sigproc(stream)
     src = torch.from_numpy(payload).cuda()
-    pitch = 1004
+    pitch = (t + 3) // 4 * 4
     dst = torch.zeros((c, pitch), device="cuda")
     torch.cuda.synchronize()
     bad = dev.sigproc_to_filterbank(src.data_ptr(), c, t, dst.data_ptr(), pitch)
     assert bad == -1
-    assert np.array_equal(dst.cpu().numpy()[:, :t], expect)
-    payload[500, 3] = np.inf
-    payload[700, 1] = np.nan
-    src = torch.from_numpy(payload).cuda()
-    torch.cuda.synchronize()
-    assert dev.sigproc_to_filterbank(src.data_ptr(), c, t, dst.data_ptr(), pitch) == 500 * c + 3
+    assert np.array_equal(_bits(dst.cpu().numpy()[:, :t]), _bits(expect))
+    if t * c > 2:
+        payload[t // 2, c // 2] = np.inf
+        payload[-1, 0] = np.nan
+        _, offset = O.ref_parse_sigproc(O.sigproc_bytes(payload, 20000, 1716.67, -0.29))
+        src = torch.from_numpy(payload).cuda()
+        torch.cuda.synchronize()
+        first = dev.sigproc_to_filterbank(src.data_ptr(), c, t, dst.data_ptr(), pitch)
+        assert header_end + 4 * first == offset
 
 
 @pytest.mark.parametrize("flags", [0, "tm", "tm-ns2", "cps3-ns4", "packed", "tm-packed",
@@ -695,3 +703,29 @@ def test_packed_stages_bit_exact(dev, cfg, depth):
     dev.synchronize()
     assert np.array_equal(_bits(ob[0].cpu().numpy()), _bits(ref))
     assert np.array_equal(_bits(ob[1].cpu().numpy()), _bits(ref * 2.0))
+
+
+def test_live_plan_survives_a_smaller_plan_of_the_same_kernel(dev):
+    """A kernel's dynamic shared-memory attribute is per function, not per
+    plan: a plan created later with narrower stages (less shared memory) on
+    the same kernel must not break the launches of a live wider plan."""
+    import torch
+    g_setup, d = api.APERTIF, 64
+    table = api.build_delay_table(g_setup, d)
+    t = api.instance_sizing(g_setup, d).num_samples
+    s, c = g_setup.samples_per_second, g_setup.channels
+    fb = api.noise_filterbank(g_setup, t, 1.0, 1)
+    x = torch.from_numpy(fb.data).cuda()
+    sh = torch.from_numpy(table.shifts.view(np.int32)).cuda()
+    ref = torch.empty((d, s), device="cuda")
+    dev.plan(sh.data_ptr(), c, d, s, t, t).execute(x.data_ptr(), ref.data_ptr())
+    wide = dev.plan(sh.data_ptr(), c, d, s, t, t, K(32, 8, 5, 1), 1, "smem",
+                    flags=15 << N.DD_CONFIG_CPS_SHIFT)
+    narrow = dev.plan(sh.data_ptr(), c, d, s, t, t, K(32, 8, 5, 1), 1, "smem",
+                      flags=(1 << N.DD_CONFIG_CPS_SHIFT) | (2 << N.DD_CONFIG_NSTAGE_SHIFT))
+    assert wide.info()["smem_bytes"] > narrow.info()["smem_bytes"]
+    for p in (wide, narrow, wide):
+        out = torch.full((d, s), float("nan"), device="cuda")
+        p.execute(x.data_ptr(), out.data_ptr())
+        dev.synchronize()
+        assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
