@@ -53,15 +53,22 @@ def gen_dispatch() -> None:
             f.write(r.stdout)
 
 
-def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, checked: bool = False,
+          defines=(), out: str = None) -> str:
     """checked=True: libdedisp_b200_checked.so, the same library with every
     staged shared-memory read, bulk copy and output store bounds-checked on
     the device (-DDDB_CHECKED; dd_debug_violations) -- the memcheck stand-in
-    (tests/test_gpu_checked.py)."""
+    (tests/test_gpu_checked.py).  defines/out: an A/B build of the same
+    sources with extra -D macros into `out` (tools/ab_build.py)."""
     gen_dispatch()
-    objdir = os.path.join(PKG, "build_checked" if checked else "build")
-    lib = LIB_CHECKED if checked else LIB
-    extra = ["-DDDB_CHECKED"] if checked else []
+    extra = (["-DDDB_CHECKED"] if checked else []) + ["-D" + d for d in defines]
+    if out:
+        tag = os.path.splitext(os.path.basename(out))[0]
+        objdir = os.path.join(PKG, "build_ab", tag)
+        lib = out
+    else:
+        objdir = os.path.join(PKG, "build_checked" if checked else "build")
+        lib = LIB_CHECKED if checked else LIB
     os.makedirs(objdir, exist_ok=True)
     deps_common = [os.path.join(CSRC, h) for h in HEADERS] + PUBLIC + [__file__]
     objs = []

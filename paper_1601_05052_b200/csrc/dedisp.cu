@@ -183,48 +183,50 @@ __device__ __forceinline__ uint64_t stage_offset(const TiledArgs& a, uint32_t sl
     return static_cast<uint64_t>(slot * a.cps) * a.win_cap;
 }
 
-// (lo, span) of the channels of chunk g (up to kMaxCps), fetched one chunk ahead
-// by the producer so the global-memory latency overlaps its slot wait.
-struct ChunkSpans {
-  uint2 v[kMaxCps];
-};
+// The producer warp.  Lane cc stages channel cc of each chunk (one bulk
+// copy per lane, in parallel); lane 0 also copies the chunk's plan records
+// and closes the phase.  Each lane keeps the (lo, span) of its channel for
+// the next kSpanAhead chunks in registers, loaded from global memory that
+// many chunks ahead: with short per-chunk work (few DMs, small d) the
+// producer otherwise waits one L2 round trip per chunk.
+constexpr int kSpanAhead = 4;
 
 template <bool PK>
-__device__ __forceinline__ ChunkSpans pipe_spans(const TiledArgs& a, const Pipe& p, uint32_t g) {
-  ChunkSpans c;
+__device__ __forceinline__ uint2 lane_span(const TiledArgs& a, const Pipe& p, uint32_t g,
+                                           uint32_t lane) {
+  if (g >= p.total) return make_uint2(0u, 0u);
   const uint32_t b = p.b_first + g / p.nchunk;
   uint32_t ch0, ncs;
   stage_channels<PK>(a, g % p.nchunk, ch0, ncs);
-  const uint2* src = a.ls + static_cast<uint64_t>(b) * a.channels + ch0;
-#pragma unroll
-  for (uint32_t cc = 0; cc < kMaxCps; ++cc) {
-    if (cc >= ncs) break;  // a branch, not kMaxCps predicated loads
-    c.v[cc] = __ldg(src + cc);
-  }
-  return c;
+  if (lane >= ncs) return make_uint2(0u, 0u);
+  return __ldg(a.ls + static_cast<uint64_t>(b) * a.channels + ch0 + lane);
 }
 
 // Stage chunk g = (tile, channel group) into its slot: one bulk copy for the
-// chunk's plan records, one per channel window, all counted on full[slot].
+// chunk's plan records (lane 0), one per channel window (lane cc), all
+// counted on full[slot].
 template <bool PK>
 __device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, uint32_t g,
-                                           const ChunkSpans& cs) {
+                                           uint2 ls, uint32_t lane) {
   const uint32_t b = p.b_first + g / p.nchunk;
   uint32_t ch0, ncs;
   stage_channels<PK>(a, g % p.nchunk, ch0, ncs);
   const uint32_t slot = g % a.nstage;
-  const uint8_t* rsrc = a.rec + (static_cast<uint64_t>(b) * a.channels + ch0) * a.rec_bytes;
   uint64_t* bar = &p.full[slot];
   // Each copy first raises the phase's expected bytes; the closing arrival
-  // (the phase's only one) cannot complete it before every copy is counted.
-  mbar_expect_tx(bar, ncs * a.rec_bytes);
-  bulk_g2s(p.recs + slot * a.cps * a.rec_bytes, rsrc, ncs * a.rec_bytes, bar);
-  const float* src = a.in + blockIdx.y * a.in_beam_stride + static_cast<uint64_t>(ch0) * a.in_pitch;
-  float* dst = p.wins + stage_offset<PK>(a, slot);
-#pragma unroll
-  for (uint32_t cc = 0; cc < kMaxCps; ++cc) {
-    if (cc >= ncs) break;
-    const uint32_t lo = cs.v[cc].x, span = cs.v[cc].y;
+  // (the phase's only one, after the warp has issued every copy) cannot
+  // complete it before every copy is counted.
+  if (lane == 0) {
+    const uint8_t* rsrc = a.rec + (static_cast<uint64_t>(b) * a.channels + ch0) * a.rec_bytes;
+    mbar_expect_tx(bar, ncs * a.rec_bytes);
+    bulk_g2s(p.recs + slot * a.cps * a.rec_bytes, rsrc, ncs * a.rec_bytes, bar);
+  }
+  if (lane < ncs) {
+    const uint32_t cc = lane;
+    const float* src =
+        a.in + blockIdx.y * a.in_beam_stride + static_cast<uint64_t>(ch0 + cc) * a.in_pitch;
+    float* dst = p.wins + stage_offset<PK>(a, slot);
+    const uint32_t lo = ls.x, span = ls.y;
     const uint32_t start = (p.t0 + lo) & ~3u;
     // a predicated last time tile must not read past the (pitched) row
     const uint32_t end = min((p.t0 + lo + span + a.tile_time + 3u) & ~3u,
@@ -235,24 +237,49 @@ __device__ __forceinline__ void pipe_issue(const TiledArgs& a, const Pipe& p, ui
     DDB_CHECK(window_offset<PK>(a, ch0, cc) + (end - start) <=
               (PK ? a.stage_floats : a.cps * a.win_cap));
     mbar_expect_tx(bar, bytes);
-    bulk_g2s(dst + window_offset<PK>(a, ch0, cc), src + static_cast<uint64_t>(cc) * a.in_pitch + start,
-             bytes, bar);
+    bulk_g2s(dst + window_offset<PK>(a, ch0, cc), src + start, bytes, bar);
   }
-  mbar_arrive(bar);
+  __syncwarp();
+  if (lane == 0) mbar_arrive(bar);
 }
 
-// The producer lane: issue every chunk as soon as its slot is handed back.
+// The producer warp: issue every chunk as soon as its slot is handed back.
 template <bool PK>
 __device__ __forceinline__ void pipe_produce(const TiledArgs& a, const Pipe& p) {
-  ChunkSpans next = pipe_spans<PK>(a, p, 0);
+  const uint32_t lane = threadIdx.x & 31;
+  uint2 ahead[kSpanAhead];
+#pragma unroll
+  for (int i = 0; i < kSpanAhead; ++i) ahead[i] = lane_span<PK>(a, p, i, lane);
   for (uint32_t g = 0; g < p.total; ++g) {
-    const ChunkSpans cur = next;
-    if (g + 1 < p.total) next = pipe_spans<PK>(a, p, g + 1);
+    const uint2 cur = ahead[0];
+#pragma unroll
+    for (int i = 0; i + 1 < kSpanAhead; ++i) ahead[i] = ahead[i + 1];
+    ahead[kSpanAhead - 1] = lane_span<PK>(a, p, g + kSpanAhead, lane);
     const uint32_t use = g / a.nstage;
     if (use > 0) mbar_wait_sleep(&p.empty[g % a.nstage], (use - 1) & 1u);
-    pipe_issue<PK>(a, p, g, cur);
+    pipe_issue<PK>(a, p, g, cur, lane);
   }
 }
+
+// Channels per unrolled step of the consumer loop (Body::kUnroll, default 1).
+template <class B, class = void>
+struct ChannelUnroll {
+  static constexpr uint32_t value = 1;
+};
+template <class B>
+struct ChannelUnroll<B, decltype(void(B::kUnroll))> {
+  static constexpr uint32_t value = B::kUnroll;
+};
+
+// Bodies that run a whole stage themselves (kStagePipe = true).
+template <class B, class = void>
+struct HasStagePipe {
+  static constexpr bool value = false;
+};
+template <class B>
+struct HasStagePipe<B, decltype(void(B::kStagePipe))> {
+  static constexpr bool value = B::kStagePipe;
+};
 
 // Warp-specialised pipeline.  The LAST warp of the CTA is the producer: one
 // lane runs ahead issuing bulk copies as soon as a slot is handed back
@@ -277,7 +304,7 @@ __device__ __forceinline__ void staged_loop_with(const TiledArgs& a, uint8_t* sm
   }
   __syncthreads();
   if (tid >= consumers * 32) {  // producer warp
-    if (tid == consumers * 32) pipe_produce<PK>(a, p);
+    pipe_produce<PK>(a, p);
     return;
   }
   // Consumer threads beyond the config's items (the block is rounded up to
@@ -303,13 +330,29 @@ __device__ __forceinline__ void staged_loop_with(const TiledArgs& a, uint8_t* sm
     body.chk.hi = wbase + (PK ? a.stage_floats : a.cps * a.win_cap);
 #endif
     if (active) {
-      for (uint32_t cc = 0; cc < ncs; ++cc) {
-        const uint32_t* r = reinterpret_cast<const uint32_t*>(rbase + cc * a.rec_bytes);
-        const float* w = wbase + window_offset<PK>(a, ch0, cc);
-        if constexpr (Body::kRowBase)
-          body.channel(r, w);
-        else
-          body.channel(r, w + ((p.t0 + r[0]) & 3u));
+      if constexpr (HasStagePipe<Body>::value) {
+        body.stage(rbase, wbase, ncs);
+      } else {
+        const auto one = [&](uint32_t cc) {
+          const uint32_t* r = reinterpret_cast<const uint32_t*>(rbase + cc * a.rec_bytes);
+          const float* w = wbase + window_offset<PK>(a, ch0, cc);
+          if constexpr (Body::kRowBase)
+            body.channel(r, w);
+          else
+            body.channel(r, w + ((p.t0 + r[0]) & 3u));
+        };
+        uint32_t cc = 0;
+        if constexpr (ChannelUnroll<Body>::value > 1) {
+          // light bodies (few accumulators: small d): U channels per step so
+          // their record and operand loads overlap instead of forming one
+          // latency chain per channel
+          constexpr uint32_t U = ChannelUnroll<Body>::value;
+          for (; cc + U <= ncs; cc += U) {
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u) one(cc + u);
+          }
+        }
+        for (; cc < ncs; ++cc) one(cc);
       }
     }
     __syncwarp();
@@ -335,6 +378,11 @@ template <int K, int W, int IT = 0, bool PK = false>
 struct SmemBody {
   static constexpr bool kRowBase = false;  // channel() gets the row at lo's sample
   static constexpr bool kPacked = PK;      // packed stages (compile time)
+#ifndef DDB_SMEM_UNROLL
+#define DDB_SMEM_UNROLL 4
+#endif
+  // few accumulators per thread (small d): unroll the channel loop
+  static constexpr uint32_t kUnroll = K * W <= 8 ? DDB_SMEM_UNROLL : 1;
   const TiledArgs& a;
   uint32_t it, id;
   float acc[K][W];
@@ -649,6 +697,17 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* r) {
                : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]),
+        "=f"(r[7]), "=f"(r[8]), "=f"(r[9]), "=f"(r[10]), "=f"(r[11]), "=f"(r[12]), "=f"(r[13]),
+        "=f"(r[14]), "=f"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
                : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3])
@@ -666,11 +725,27 @@ __device__ __forceinline__ void tmem_wait_ld() {
 #ifndef DDB_TMEM_GROUP
 #define DDB_TMEM_GROUP 4
 #endif
+#ifndef DDB_TMEM_READ16
+#define DDB_TMEM_READ16 0
+#endif
+// launch bound of k_tmemwin: 288 threads (up to 8 consumer warps), or an A/B
+// build bounded to 160 threads x 2 CTAs (<= 204 registers)
+#ifndef DDB_TMEM_LB2
+#define DDB_TMEM_LB2 0
+#endif
+// software-pipelined stages: channel c+1's window loads (LDS) are issued
+// before channel c's TMEM reads and adds, and land in a second TMEM column
+// block, so the window stores no longer wait on the shared-memory loads
+#ifndef DDB_TMEM_PIPE
+#define DDB_TMEM_PIPE 0
+#endif
 
 template <int K, int W, int SPAN, int COLS, bool FULL_HEAD = true>
 struct TmemBody {
   static constexpr bool kRowBase = true;  // channel() gets the 16-byte aligned row start
   static constexpr bool kPacked = false;
+  static constexpr bool kStagePipe = DDB_TMEM_PIPE != 0;
+  static constexpr int kBufs = kStagePipe ? 2 : 1;  // TMEM window blocks per warp
   static_assert(W % 4 == 0, "16-byte window loads (W/4 odd is conflict-free, even is 2-way)");
   static_assert(COLS == 32 || COLS == 64, "32 or 64 TMEM columns per warp window");
   static_assert(W + SPAN + 3 <= COLS, "window must fit the warp's TMEM columns");
@@ -696,7 +771,7 @@ struct TmemBody {
     col = ((warp % warps_time) * 32 + lane) * W;
     dml = (warp / warps_time) * K;
     // lanes (warp % 4) * 32.. are this warp's TMEM rows; COLS columns per warp
-    taddr = tmem_base + (((warp & 3) * 32) << 16) + (warp >> 2) * COLS;
+    taddr = tmem_base + (((warp & 3) * 32) << 16) + (warp >> 2) * COLS * kBufs;
   }
   __device__ __forceinline__ void zero() {
 #pragma unroll
@@ -773,8 +848,9 @@ struct TmemBody {
   }
 
   // Window -> this lane's TMEM row; afterwards n.win may be refilled.
-  __device__ __forceinline__ void commit(Pre& n) const {
+  __device__ __forceinline__ void commit(Pre& n, uint32_t buf = 0) const {
     if (n.nv == 0) return;
+    const uint32_t taddr = this->taddr + buf;
     tmem_st32(taddr, n.win);
     if constexpr (kTail > 0) {
       // columns 32.. of the widest window (alignment + SPAN + W): an x8,
@@ -801,21 +877,30 @@ struct TmemBody {
   }
 
   __device__ __forceinline__ void accumulate(const uint32_t (&off)[K], bool fast,
-                                             const float* base) {
+                                             const float* base, uint32_t buf = 0) {
+    const uint32_t taddr = this->taddr + buf;
     if (fast) {
       // (ptxas schedules the loads itself: with the staging registers free
       // between channels it keeps 3-4 of them in flight).  G DMs' TMEM reads
       // per wait::ld (DDB_TMEM_GROUP, A/B builds).
       constexpr int G = (DDB_TMEM_GROUP <= K && K % DDB_TMEM_GROUP == 0) ? DDB_TMEM_GROUP : 2;
+      // W = 12 read as one x16 (4 columns wasted: the window has the slack)
+      // -- one TMEM address (R2UR) and one LDTM per DM instead of two
+      constexpr bool kRead16 = DDB_TMEM_READ16 && W == 12 && SPAN + 3 + 16 <= COLS;
+      constexpr int WB = kRead16 ? 16 : W;
 #pragma unroll
       for (int k = 0; k < K; k += G) {
-        float v[G][W];
+        float v[G][WB];
 #pragma unroll
         for (int h = 0; h < G; ++h) {
           const uint32_t c = taddr + off[k + h];
+          if constexpr (kRead16) {
+            tmem_ld16(c, v[h]);
+          } else {
 #pragma unroll
-          for (int j = 0; j + 8 <= W; j += 8) tmem_ld8(c + j, &v[h][j]);
-          if constexpr (W % 8 == 4) tmem_ld4(c + (W - W % 8), &v[h][W - W % 8]);
+            for (int j = 0; j + 8 <= W; j += 8) tmem_ld8(c + j, &v[h][j]);
+            if constexpr (W % 8 == 4) tmem_ld4(c + (W - W % 8), &v[h][W - W % 8]);
+          }
         }
         tmem_wait_ld();
 #pragma unroll
@@ -853,6 +938,27 @@ struct TmemBody {
     commit(n);
     accumulate(n.off, n.nv != 0, n.base);
   }
+  // kStagePipe: the channels of one stage (fixed slots of win_cap floats),
+  // two at a time -- fetch(c+1) | accumulate(c) | commit(c+1) -- alternating
+  // between the two TMEM column blocks
+  __device__ __forceinline__ void stage(const uint8_t* rbase, const float* wbase, uint32_t ncs) {
+    const auto rec = [&](uint32_t cc) {
+      return reinterpret_cast<const uint32_t*>(rbase + cc * a.rec_bytes);
+    };
+    Pre A, B;
+    fetch(A, rec(0), wbase);
+    commit(A, 0);
+    for (uint32_t cc = 0; cc < ncs; cc += 2) {
+      const bool more1 = cc + 1 < ncs, more2 = cc + 2 < ncs;
+      if (more1) fetch(B, rec(cc + 1), wbase + (cc + 1) * a.win_cap);
+      accumulate(A.off, A.nv != 0, A.base, 0);
+      if (!more1) break;
+      commit(B, COLS);
+      if (more2) fetch(A, rec(cc + 2), wbase + (cc + 2) * a.win_cap);
+      accumulate(B.off, B.nv != 0, B.base, COLS);
+      if (more2) commit(A, 0);
+    }
+  }
   __device__ __forceinline__ void load(uint32_t dm0, uint32_t t0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -888,7 +994,7 @@ __device__ __forceinline__ void tmemwin_run(const TiledArgs& a) {
   __shared__ uint32_t tmem_base;
   const uint32_t consumers = blockDim.x / 32 - 1;
   using Body = TmemBody<K, W, SPAN, COLS, FULL_HEAD>;
-  const uint32_t cols = tmem_cols_for(consumers, COLS);
+  const uint32_t cols = tmem_cols_for(consumers, COLS * Body::kBufs);
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_addr(&tmem_base)),
@@ -908,8 +1014,13 @@ __device__ __forceinline__ void tmemwin_run(const TiledArgs& a) {
                  : "memory");
 }
 
+#if DDB_TMEM_LB2
+template <int K, int W, int SPAN, int COLS>
+__global__ void __maxnreg__(DDB_TMEM_LB2) k_tmemwin(const TiledArgs a) {
+#else
 template <int K, int W, int SPAN, int COLS>
 __global__ void __launch_bounds__(288) k_tmemwin(const TiledArgs a) {
+#endif
   tmemwin_run<K, W, SPAN, COLS>(a);
 }
 

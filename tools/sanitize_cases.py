@@ -51,7 +51,8 @@ def main():
             (K(160, 1, 5, 8), 2, "smem", N.DD_CONFIG_TIME_MAJOR),
         ]),
         ("LOFAR-like", api.ObservationSetup("lofarish", 20000, 32, 138.0, 0.19, 0.0, 0.25), 32, [
-            (K(160, 1, 10, 4), 2, "smem", N.DD_CONFIG_PACKED_STAGES | N.DD_CONFIG_TIME_MAJOR),
+            (K(160, 1, 10, 4), 2, "smem",
+             N.DD_CONFIG_PACKED_STAGES | N.DD_CONFIG_TIME_MAJOR | N.DD_CONFIG_GPU_TILING),
             (K(32, 4, 5, 2), 1, "smem", 15 << 8),
         ]),
     ]

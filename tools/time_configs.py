@@ -5,6 +5,7 @@
 Extra fields: "g" requests GPU tiling (tile_time need not divide s),
 "cpsN" pins N channels per pipeline stage, "occ" the TMEM three-CTA build,
 "nsN" N pipeline stages, "tm" time-major CTA raster, "pk" packed stages.
+--cold flushes L2 before every timed run (dd_plan_time_ex).
 """
 import os
 import sys
@@ -18,6 +19,8 @@ from paper_1601_05052_b200 import api  # noqa: E402
 
 
 def main():
+    cold = "--cold" in sys.argv
+    sys.argv = [a for a in sys.argv if a != "--cold"]
     setup = api.find_builtin(sys.argv[1])
     d = int(sys.argv[2])
     c, s = setup.channels, setup.samples_per_second
@@ -45,7 +48,7 @@ def main():
         except ValueError as e:
             print(f"{spec:28s} invalid: {e}")
             continue
-        runs = p.time(x.data_ptr(), out.data_ptr(), warmup=2, repeats=10)
+        runs = p.time(x.data_ptr(), out.data_ptr(), warmup=2, repeats=10, flush_l2=cold)
         ms = sorted(runs)[len(runs) // 2] * 1e3
         i = p.info()
         print(f"{spec:28s} {i['family']:7s} {ms:8.3f} ms  {flop / ms / 1e6:9.1f} GFLOP/s  "
