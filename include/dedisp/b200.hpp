@@ -171,6 +171,7 @@ enum class Staging : std::uint32_t {
   Direct = DD_STAGING_DIRECT,
   RegisterWindow = DD_STAGING_REGWIN,
   TensorMemory = DD_STAGING_TMEM,
+  Rectangle = DD_STAGING_RECT,
 };
 
 struct ExecOptions {

@@ -66,7 +66,9 @@ typedef enum dd_staging {
   DD_STAGING_SMEM = 1,   /* per-channel windows staged by TMA bulk copies   */
   DD_STAGING_DIRECT = 2, /* loads straight from global through L1/L2       */
   DD_STAGING_REGWIN = 3, /* TMA-staged windows + per-thread register window */
-  DD_STAGING_TMEM = 4    /* TMA-staged windows + per-lane TMEM windows (tcgen05) */
+  DD_STAGING_TMEM = 4,   /* TMA-staged windows + per-lane TMEM windows (tcgen05) */
+  DD_STAGING_RECT = 5    /* one 3-D TMA box per channel group (small spans: small d);
+                            channels per stage = 16 x DD_CONFIG_CPS (0: plan's choice) */
 } dd_staging;
 
 /* KernelConfig (kernels.hpp:40-52) plus the two GPU knobs of the north star:

@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DDB_LIB") or os.path.join(PKG, "libdedisp_b200.so")
 
 DD_OK, DD_ERR_INVALID_ARGUMENT, DD_ERR_CAPACITY, DD_ERR_CUDA, DD_ERR_NO_DEVICE, DD_ERR_INTERNAL = range(6)
-STAGING = {"auto": 0, "smem": 1, "direct": 2, "regwin": 3, "tmem": 4}
+STAGING = {"auto": 0, "smem": 1, "direct": 2, "regwin": 3, "tmem": 4, "rect": 5}
 STAGING_NAME = {v: k for k, v in STAGING.items()}
 DD_CONFIG_GPU_TILING = 0x1
 DD_CONFIG_HIGH_OCCUPANCY = 0x2

@@ -9,6 +9,8 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -383,7 +385,7 @@ dd_status dd_validate_config(const dd_config* k, uint32_t num_dms, uint32_t s,
   if (static_cast<uint64_t>(k->work_time) * k->work_dm > L.max_accumulators)
     return fail(DD_ERR_INVALID_ARGUMENT, "work_time * work_dm exceeds the accumulator limit of " +
                                              std::to_string(L.max_accumulators));
-  if (k->staging > DD_STAGING_TMEM) return fail(DD_ERR_INVALID_ARGUMENT, "unknown staging mode");
+  if (k->staging > DD_STAGING_RECT) return fail(DD_ERR_INVALID_ARGUMENT, "unknown staging mode");
   if (k->flags & ~(DD_CONFIG_GPU_TILING | DD_CONFIG_HIGH_OCCUPANCY | DD_CONFIG_TIME_MAJOR |
                    DD_CONFIG_PACKED_STAGES | DD_CONFIG_CPS_MASK | DD_CONFIG_NSTAGE_MASK))
     return fail(DD_ERR_INVALID_ARGUMENT, "unknown config flags");
@@ -495,6 +497,8 @@ bool smem_geometry(const dd_context* c, uint32_t tile_time, uint32_t tile_dm, ui
 }
 
 void free_plan_buffers(dd_plan* p) {
+  cudaFree(p->d_glo);
+  p->d_glo = nullptr;
   cudaFree(p->d_rec);
   cudaFree(p->d_ls);
   cudaFree(p->d_chan_span);
@@ -565,6 +569,134 @@ cudaError_t pack_stages(dd_context* c, dd_plan* p, ddb::TiledArgs& a, uint32_t c
   return cudaSuccess;
 }
 
+// ---------------------------------------------------- K6 rectangles --
+// cuTensorMapEncodeTiled from the driver (through the runtime's entry-point
+// query: no libcuda link needed).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// The 3-D view (samples, channels, beams) of the input a rectangle plan
+// loads boxes of rect_w samples x rect_ch channels from; re-encoded only
+// when the input pointer or the beam layout changes.
+dd_status rect_tensor_map(dd_plan* p, const float* d_in, uint32_t beams, uint64_t beam_stride) {
+  if (p->tmap_in == d_in && p->tmap_beams == beams && p->tmap_beam_stride == beam_stride)
+    return DD_OK;
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (enc == nullptr) return fail(DD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const ddb::TiledArgs& a = p->args;
+  cuuint64_t dims[3] = {a.in_pitch, a.channels, beams};
+  cuuint64_t strides[2] = {a.in_pitch * 4ull,
+                           beams > 1 ? beam_stride * 4ull : a.in_pitch * 4ull * a.channels};
+  cuuint32_t box[3] = {a.rect_w, a.rect_ch, 1u};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  const CUresult r =
+      enc(&p->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(d_in), dims, strides,
+          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(DD_ERR_INVALID_ARGUMENT,
+                "staging=rect: cuTensorMapEncodeTiled rejected the input view (error " +
+                    std::to_string(static_cast<int>(r)) + ")");
+  p->tmap_in = d_in;
+  p->tmap_beams = beams;
+  p->tmap_beam_stride = beam_stride;
+  return DD_OK;
+}
+
+// Plan the rectangle family: channel groups of rect_ch (16 x DD_CONFIG_CPS,
+// else the widest of 128/64/32/16/8 whose stages fit), the group lows and
+// offsets from k_plan_rect, and a box rect_w = tile_time + widest group span
+// (<= 256 samples, the TMA box limit -- wider spans are not this family's).
+dd_status plan_rect(dd_context* c, dd_plan* p, const dd_config* k, uint32_t channels,
+                    uint64_t in_pitch) {
+  ddb::TiledArgs& a = p->args;
+  const uint64_t block = static_cast<uint64_t>(k->items_time) * k->items_dm;
+  if (in_pitch % 4 != 0) return fail(DD_ERR_INVALID_ARGUMENT, "staging=rect: input pitch % 4 != 0");
+  if (block > 1024) return fail(DD_ERR_INVALID_ARGUMENT, "staging=rect: more than 1024 threads");
+  ddb::RectFn fn = ddb::find_rect_kernel(k->work_dm, k->work_time, k->items_time);
+  if (fn == nullptr)
+    return fail(DD_ERR_INVALID_ARGUMENT,
+                "staging=rect: no work_dm x work_time variant (1..16 x 1..4 instantiated)");
+  if (tensor_map_encoder() == nullptr) return fail(DD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const uint32_t want = ((k->flags & DD_CONFIG_CPS_MASK) >> DD_CONFIG_CPS_SHIFT) * 16u;
+  uint32_t ns = (k->flags & DD_CONFIG_NSTAGE_MASK) >> DD_CONFIG_NSTAGE_SHIFT;
+  if (ns < 2) ns = 4;
+  std::vector<uint32_t> tries;
+  if (want) tries.push_back(want);
+  else tries = {128u, 64u, 32u, 16u, 8u};
+  for (uint32_t rc : tries) {
+    rc = std::min(rc, channels);
+    const uint32_t groups = (channels + rc - 1) / rc;
+    const uint32_t rec_words = (rc * a.tile_dm + 3u) & ~3u;
+    cudaError_t e = cudaMalloc(&p->d_glo, static_cast<uint64_t>(a.tiles_dm) * groups * 4);
+    if (e == cudaSuccess)
+      e = cudaMalloc(&p->d_rec, static_cast<uint64_t>(a.tiles_dm) * groups * rec_words * 4);
+    uint32_t maxw = 0;
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->d_scratch, 0, 4, c->stream);
+    if (e == cudaSuccess)
+      e = ddb::launch_plan_rect(a.shifts, p->d_glo, reinterpret_cast<uint32_t*>(p->d_rec),
+                                c->d_scratch, channels, a.tiles_dm, a.tile_dm, rc, groups,
+                                rec_words, c->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(&maxw, c->d_scratch, 4, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+      free_plan_buffers(p);
+      return cuda_fail(e, "rect pre-pass");
+    }
+    // + 3: the box starts at the aligned sample at or below the group low
+    const uint64_t w = (static_cast<uint64_t>(a.tile_time) + maxw + 3u + 3u) & ~3ull;
+    if (w > 256) {
+      free_plan_buffers(p);
+      return fail(DD_ERR_INVALID_ARGUMENT,
+                  "staging=rect: tile_time + the widest group span = " + std::to_string(w) +
+                      " samples exceeds the 256-sample TMA box (a small-d family)");
+    }
+    const uint64_t stage = ((rc * w * 4 + 127) & ~127ull) + ((rec_words * 4ull + 127) & ~127ull);
+    const uint64_t smem = ddb::kPipeHeader + ns * stage;
+    if (smem > static_cast<uint64_t>(c->smem_optin)) {
+      free_plan_buffers(p);
+      if (want) return fail(DD_ERR_INVALID_ARGUMENT, "staging=rect: stages do not fit shared memory");
+      continue;
+    }
+    a.rect_w = static_cast<uint32_t>(w);
+    a.rect_ch = rc;
+    a.rect_groups = groups;
+    a.rec = p->d_rec;
+    a.rec_bytes = rec_words * 4;
+    a.glo = p->d_glo;
+    a.nstage = ns;
+    a.cps = rc;
+    a.win_cap = a.rect_w;
+    a.packed = 0;
+    p->rect_fn = fn;
+    p->smem = static_cast<uint32_t>(smem);
+    p->threads = static_cast<uint32_t>(((block + 31) & ~31ull) + 32);
+    p->blocks = static_cast<uint32_t>(((a.tiles_dm + a.depth - 1) / a.depth) * a.tiles_time);
+    p->family = DD_STAGING_RECT;
+    p->max_span = maxw;
+    p->staged_bytes = 4ull * a.tiles_time * a.tiles_dm * groups * rc * a.rect_w;
+    e = ddb::prepare_rect(fn, p->smem);
+    if (e != cudaSuccess) {
+      free_plan_buffers(p);
+      return cuda_fail(e, "cudaFuncSetAttribute");
+    }
+    return DD_OK;
+  }
+  return fail(DD_ERR_INVALID_ARGUMENT, "staging=rect: no channel group width fits shared memory");
+}
+
 dd_status max_of_device_table(dd_context* c, const uint32_t* d_shifts, uint64_t n, uint32_t* out) {
   DD_CUDA(cudaMemsetAsync(c->d_scratch, 0, 4, c->stream));
   DD_CUDA(launch_max_u32(d_shifts, n, c->d_scratch, c->stream));
@@ -595,6 +727,12 @@ dd_status dd_config_family(dd_context* c, const dd_config* k, uint32_t channels,
   switch (k->staging) {
     case DD_STAGING_AUTO:
       *family = smem_ok ? DD_STAGING_SMEM : regwin_ok ? DD_STAGING_REGWIN : DD_STAGING_DIRECT;
+      return DD_OK;
+    case DD_STAGING_RECT:
+      if (find_rect_kernel(k->work_dm, k->work_time, k->items_time) == nullptr || block > 1024)
+        return fail(DD_ERR_INVALID_ARGUMENT,
+                    "staging=rect: no work_dm x work_time variant or more than 1024 threads");
+      *family = DD_STAGING_RECT;
       return DD_OK;
     case DD_STAGING_TMEM:
       if (!tmem_shape_ok(k->work_dm, k->work_time, k->items_time, block))
@@ -689,6 +827,16 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
         num_dms, 2.0 * c->sm_count * a.tile_dm * std::max<uint32_t>(1, a.depth));
     const double window = a.tile_time + static_cast<double>(md) * resident_dms / num_dms;
     if (4.0 * channels * window > 0.75 * c->l2_bytes) a.time_major = 1;
+  }
+
+  if (k->staging == DD_STAGING_RECT) {
+    const dd_status st = plan_rect(c, p, k, channels, in_pitch);
+    if (st != DD_OK) {
+      delete p;
+      return st;
+    }
+    *out = p;
+    return DD_OK;
   }
 
   const uint64_t block = static_cast<uint64_t>(k->items_time) * k->items_dm;
@@ -836,7 +984,7 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
 
 dd_status dd_plan_destroy(dd_plan* p) {
   if (p == nullptr) return DD_OK;
-  if (p->d_rec) {
+  if (p->d_rec || p->d_glo) {
     cudaSetDevice(p->ctx->device);
     free_plan_buffers(p);
   }
@@ -860,11 +1008,13 @@ dd_status dd_plan_get_info(const dd_plan* p, dd_plan_info* info) {
   info->staged_bytes = p->staged_bytes;
   info->time_major = p->args.time_major;
   info->packed_stages = p->args.packed ? p->args.packed_stages : 0;
-  if (p->smem_fn != nullptr) {
+  const void* kfn = p->smem_fn ? reinterpret_cast<const void*>(p->smem_fn)
+                               : reinterpret_cast<const void*>(p->rect_fn);
+  if (kfn != nullptr) {
     cudaFuncAttributes fa{};
     int ctas = 0;
-    if (cudaFuncGetAttributes(&fa, p->smem_fn) == cudaSuccess) info->registers = fa.numRegs;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, p->smem_fn, static_cast<int>(p->threads),
+    if (cudaFuncGetAttributes(&fa, kfn) == cudaSuccess) info->registers = fa.numRegs;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kfn, static_cast<int>(p->threads),
                                                       p->smem) == cudaSuccess)
       info->ctas_per_sm = static_cast<uint32_t>(ctas);
   }
@@ -891,8 +1041,13 @@ dd_status dd_plan_execute(dd_plan* p, const float* d_in, float* d_out, uint64_t 
   a.in = d_in;
   a.out = d_out;
   a.out_pitch = out_pitch;
-  if (p->family == DD_STAGING_SMEM || p->family == DD_STAGING_REGWIN ||
-      p->family == DD_STAGING_TMEM) {
+  if (p->family == DD_STAGING_RECT) {
+    if ((reinterpret_cast<uintptr_t>(d_in) & 15u) != 0)
+      return fail(DD_ERR_INVALID_ARGUMENT, "staged kernels need a 16-byte aligned input");
+    DD_TRY(rect_tensor_map(p, d_in, 1, 0));
+    DD_CUDA(launch_rect(p->rect_fn, p->tmap, a, p->blocks, p->threads, p->smem, c->stream, 1));
+  } else if (p->family == DD_STAGING_SMEM || p->family == DD_STAGING_REGWIN ||
+             p->family == DD_STAGING_TMEM) {
     if ((reinterpret_cast<uintptr_t>(d_in) & 15u) != 0)
       return fail(DD_ERR_INVALID_ARGUMENT, "staged kernels need a 16-byte aligned input");
     DD_CUDA(launch_smem(p->smem_fn, a, p->blocks, p->threads, p->smem, c->stream));
@@ -923,6 +1078,11 @@ dd_status dd_plan_execute_channels(dd_plan* p, const float* d_in, float* d_out,
   a.ch_begin = ch_begin;
   a.ch_end = ch_end;
   a.accumulate = accumulate ? 1u : 0u;
+  if (p->family == DD_STAGING_RECT) {
+    DD_TRY(rect_tensor_map(p, d_in, 1, 0));
+    DD_CUDA(launch_rect(p->rect_fn, p->tmap, a, p->blocks, p->threads, p->smem, c->stream, 1));
+    return DD_OK;
+  }
   ddb::KernelFn fn = p->smem_fn;
   if (a.packed && (ch_begin != 0 || ch_end != a.channels)) {
     // packed stages cover the full channel range; a sub-range runs the fixed
@@ -959,6 +1119,12 @@ dd_status dd_plan_execute_beams(dd_plan* p, uint32_t beams, const float* d_in,
   a.out_pitch = out_pitch;
   a.in_beam_stride = in_beam_stride;
   a.out_beam_stride = out_beam_stride;
+  if (p->family == DD_STAGING_RECT) {
+    DD_TRY(rect_tensor_map(p, d_in, beams, in_beam_stride));
+    DD_CUDA(launch_rect(p->rect_fn, p->tmap, a, p->blocks, p->threads, p->smem, c->stream,
+                        beams));
+    return DD_OK;
+  }
   DD_CUDA(launch_smem(p->smem_fn, a, p->blocks, p->threads, p->smem, c->stream, beams));
   return DD_OK;
 }
@@ -981,9 +1147,14 @@ dd_status dd_plan_time_ex(dd_plan* p, const float* d_in, float* d_out, uint64_t 
   }
   for (uint32_t i = 0; i < warmup; ++i) DD_TRY(dd_plan_execute(p, d_in, d_out, out_pitch));
   for (uint32_t i = 0; i < repeats; ++i) {
-    // evict the instance from L2 outside the timed region (a memset of a
-    // buffer twice the L2 size), as bench.py does between its steps
-    if (flush_l2) DD_CUDA(cudaMemsetAsync(c->d_flush, i & 0xff, c->flush_bytes, c->stream));
+    // evict the instance from L2 outside the timed region (write a buffer
+    // twice the L2 size, then read it back so the lines left are clean: the
+    // timed kernel must not pay for writing the flush data back), as
+    // bench.py does between its steps
+    if (flush_l2) {
+      DD_CUDA(cudaMemsetAsync(c->d_flush, i & 0xff, c->flush_bytes, c->stream));
+      DD_CUDA(launch_flush_read(c->d_flush, c->flush_bytes, c->d_scratch + 3, c->stream));
+    }
     DD_CUDA(cudaEventRecord(c->ev_start, c->stream));
     DD_TRY(dd_plan_execute(p, d_in, d_out, out_pitch));
     DD_CUDA(cudaEventRecord(c->ev_stop, c->stream));

@@ -110,6 +110,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// 3-D TMA tile load global -> shared (SASS: UTMALDG), completion counted on
+// `bar` in bytes; coordinates are signed element indices, out-of-range
+// elements are zero-filled.  `tmap` is the generic address of a
+// __grid_constant__ CUtensorMap kernel parameter.
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int32_t c0, int32_t c1,
+                                            int32_t c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_addr(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar))
+      : "memory");
+}
+
 // Two IEEE round-to-nearest fp32 adds in one instruction (SASS: FADD2).
 // Each lane is an independent correctly-rounded add, so the per-output
 // accumulation order (and hence bit-exactness) is unchanged.
@@ -188,6 +201,11 @@ struct TiledArgs {
   // block and output rows at these strides (floats) -- the deployment's
   // many-beams-per-GPU batching
   uint64_t in_beam_stride, out_beam_stride;
+  // rectangle family (K6, small spans): per stage one TMA box of rect_ch
+  // channels x rect_w samples starting at t0 + glo[dm tile][group]; plan
+  // records hold, per channel, every DM's offset from the group's lo
+  const uint32_t* glo;  // [tiles_dm][groups] lowest shift of the group
+  uint32_t rect_w, rect_ch, rect_groups;
 };
 
 }  // namespace ddb

@@ -11,6 +11,8 @@
 #include <mutex>
 #include <utility>
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "regwin_dispatch.cuh"
 
@@ -1031,6 +1033,197 @@ __global__ void __launch_bounds__(160, 3) k_tmemwin_occ(const TiledArgs a) {
   tmemwin_run<K, W, SPAN, COLS, false>(a);  // predicated head: fewer live registers
 }
 
+// ---------------------------------------------------------------------
+// K6: rectangles (staging "rect") for instances whose DM tiles span few
+// samples per channel -- small d.  There the per-channel 1-D bulk copies of
+// the staged family are tiny (T + span floats) and the CTA waits on one
+// chunk's copies after another: copy count and latency, not bytes, set the
+// time.  K6 stages a whole channel group per TMA operation instead: one
+// 3-D tile load (samples x channels x beam) of the rectangle
+// [t0 + lo_g, t0 + lo_g + rect_w) x [ch0, ch0 + rect_ch), lo_g the lowest
+// shift of the group in the DM tile, so a stage is ONE copy of up to
+// rect_ch x rect_w floats (rect_w <= 256, the TMA box limit), plus one bulk
+// copy of the group's offsets.  The adds are K3's (SmemBody mapping: one
+// shared-memory operand per add, channels ascending, one fp32 accumulator
+// per output -- bit-exact).
+// ---------------------------------------------------------------------
+template <int K, int W, int IT>
+struct RectBody {
+  const TiledArgs& a;
+  uint32_t it, id;
+  float acc[K][W];
+  __device__ __forceinline__ uint32_t stride() const { return IT > 0 ? IT : a.items_time; }
+  __device__ RectBody(const TiledArgs& args) : a(args) {
+    it = threadIdx.x % stride();
+    id = threadIdx.x / stride();
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int j = 0; j < W; ++j) acc[k][j] = 0.0f;
+  }
+  // row: this channel's rectangle row (sample t0 + lo_g at index 0);
+  // off: the channel's offsets (shift - lo_g) of the tile's DMs
+  __device__ __forceinline__ void channel(const uint32_t* off, const float* row) {
+    row += it;
+    const float* p[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) p[k] = row + off[id + k * a.items_dm];
+#pragma unroll
+    for (int n = 0; n + 1 < K * W; n += 2) {
+      const int k0 = n / W, j0 = n % W, k1 = (n + 1) / W, j1 = (n + 1) % W;
+      const float2 r = fadd2(make_float2(acc[k0][j0], acc[k1][j1]),
+                             make_float2(p[k0][j0 * stride()], p[k1][j1 * stride()]));
+      acc[k0][j0] = r.x;
+      acc[k1][j1] = r.y;
+    }
+    if ((K * W) & 1) acc[K - 1][W - 1] += p[K - 1][(W - 1) * stride()];
+  }
+  __device__ __forceinline__ void load(uint32_t dm0, uint32_t t0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const float* o =
+          beam_out(a) + static_cast<uint64_t>(dm0 + id + k * a.items_dm) * a.out_pitch + t0 + it;
+#pragma unroll
+      for (int j = 0; j < W; ++j)
+        acc[k][j] = t0 + it + j * stride() < a.s ? o[j * stride()] : 0.0f;
+    }
+  }
+  __device__ __forceinline__ void store(uint32_t dm0, uint32_t t0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      DDB_CHECK(dm0 + id + k * a.items_dm < a.num_dms);
+      float* o =
+          beam_out(a) + static_cast<uint64_t>(dm0 + id + k * a.items_dm) * a.out_pitch + t0 + it;
+#pragma unroll
+      for (int j = 0; j < W; ++j)
+        if (t0 + it + j * stride() < a.s) o[j * stride()] = acc[k][j];
+    }
+  }
+};
+
+template <int K, int W, int IT>
+__global__ void __launch_bounds__(1024 + 32) k_rect(const __grid_constant__ CUtensorMap tmap,
+                                                    const TiledArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + 64);
+  // stage s: rect_ch x rect_w floats (128-byte aligned), then the offsets
+  // (rec_bytes: a group's offsets, rect_ch x tile_dm u32 padded to 16 B)
+  const uint32_t box_bytes = a.rect_ch * a.rect_w * 4u;
+  const uint32_t stage_bytes = ((box_bytes + 127u) & ~127u) + ((a.rec_bytes + 127u) & ~127u);
+  uint8_t* stages = smem + kPipeHeader;
+  const uint32_t groups_dm = (a.tiles_dm + a.depth - 1) / a.depth;
+  uint32_t t0, b_first;
+  if (a.time_major) {
+    t0 = (blockIdx.x % a.tiles_time) * a.tile_time;
+    b_first = (blockIdx.x / a.tiles_time) * a.depth;
+  } else {
+    t0 = (blockIdx.x / groups_dm) * a.tile_time;
+    b_first = (blockIdx.x % groups_dm) * a.depth;
+  }
+  const uint32_t ntiles = min(a.depth, a.tiles_dm - b_first);
+  const uint32_t g_begin = a.ch_begin / a.rect_ch;
+  const uint32_t g_end = (a.ch_end + a.rect_ch - 1) / a.rect_ch;
+  const uint32_t nchunk = g_end - g_begin;
+  const uint32_t total = ntiles * nchunk;
+  const uint32_t consumers = blockDim.x / 32 - 1;
+  if (threadIdx.x == 0) {
+    for (uint32_t q = 0; q < a.nstage; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], consumers);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x >= consumers * 32) {  // producer warp: lane 0 issues
+    if ((threadIdx.x & 31) != 0) return;
+    for (uint32_t g = 0; g < total; ++g) {
+      const uint32_t slot = g % a.nstage, use = g / a.nstage;
+      if (use > 0) mbar_wait_sleep(&empty[slot], (use - 1) & 1u);
+      const uint32_t b = b_first + g / nchunk, grp = g_begin + g % nchunk;
+      // the box starts at the 16-byte aligned sample at or below t0 + lo_g
+      // (TMA tile loads fault on an unaligned row start); the consumers add
+      // the misalignment back
+      const int32_t x0 =
+          static_cast<int32_t>((t0 + __ldg(a.glo + b * a.rect_groups + grp)) & ~3u);
+      uint8_t* st = stages + slot * stage_bytes;
+      uint64_t* bar = &full[slot];
+      mbar_expect_tx(bar, box_bytes + a.rec_bytes);
+      tma_load_3d(st, &tmap, x0, static_cast<int32_t>(grp * a.rect_ch),
+                  static_cast<int32_t>(blockIdx.y), bar);
+      bulk_g2s(st + ((box_bytes + 127u) & ~127u),
+               a.rec + (static_cast<uint64_t>(b) * a.rect_groups + grp) * a.rec_bytes, a.rec_bytes,
+               bar);
+      mbar_arrive(bar);
+    }
+    return;
+  }
+  const bool active = threadIdx.x < a.items_time * a.items_dm;
+  RectBody<K, W, IT> body(a);
+  for (uint32_t g = 0; g < total; ++g) {
+    const uint32_t q = g % nchunk, slot = g % a.nstage;
+    const uint32_t dm0 = (b_first + g / nchunk) * a.tile_dm;
+    if (q == 0) {
+      if (a.accumulate && active)
+        body.load(dm0, t0);
+      else
+        body.zero();
+    }
+    mbar_wait(&full[slot], (g / a.nstage) & 1u);
+    const uint8_t* st = stages + slot * stage_bytes;
+    const uint32_t grp0 = g_begin + q;
+    const float* rows = reinterpret_cast<const float*>(st) +
+                        ((t0 + __ldg(a.glo + (b_first + g / nchunk) * a.rect_groups + grp0)) & 3u);
+    const uint32_t* offs = reinterpret_cast<const uint32_t*>(st + ((box_bytes + 127u) & ~127u));
+    const uint32_t grp = grp0;
+    // this launch's channels of the group (a channel-range pass may start or
+    // end inside one)
+    const uint32_t c_lo = max(a.ch_begin, grp * a.rect_ch) - grp * a.rect_ch;
+    const uint32_t c_hi = min(a.ch_end, (grp + 1) * a.rect_ch) - grp * a.rect_ch;
+    if (active) {
+      uint32_t cc = c_lo;
+      constexpr uint32_t U = K * W <= 8 ? 4 : 1;
+      if constexpr (U > 1) {
+        for (; cc + U <= c_hi; cc += U) {
+#pragma unroll
+          for (uint32_t u = 0; u < U; ++u)
+            body.channel(offs + (cc + u) * a.tile_dm, rows + (cc + u) * a.rect_w);
+        }
+      }
+      for (; cc < c_hi; ++cc) body.channel(offs + cc * a.tile_dm, rows + cc * a.rect_w);
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot]);
+    if (active && q == nchunk - 1) body.store(dm0, t0);
+  }
+}
+
+using RectFn = void (*)(const CUtensorMap, const TiledArgs);
+
+struct RectVariant {
+  int k, w, it;
+  RectFn fn;
+};
+#define DDB_RV(K, W, I) {K, W, I, k_rect<K, W, I>}
+static const RectVariant kRectVariants[] = {
+    DDB_RV(1, 1, 0), DDB_RV(1, 2, 0), DDB_RV(1, 4, 0), DDB_RV(2, 1, 0), DDB_RV(2, 2, 0),
+    DDB_RV(2, 4, 0), DDB_RV(4, 1, 0), DDB_RV(4, 2, 0), DDB_RV(4, 4, 0), DDB_RV(8, 1, 0),
+    DDB_RV(8, 2, 0), DDB_RV(8, 4, 0), DDB_RV(16, 1, 0), DDB_RV(16, 2, 0),
+};
+#undef DDB_RV
+
+RectFn find_rect_kernel(uint32_t k, uint32_t w, uint32_t items_time) {
+  const RectVariant* generic = nullptr;
+  for (const RectVariant& v : kRectVariants) {
+    if (static_cast<uint32_t>(v.k) != k || static_cast<uint32_t>(v.w) != w) continue;
+    if (v.it == 0 && generic == nullptr) generic = &v;
+    if (items_time != 0 && static_cast<uint32_t>(v.it) == items_time) return v.fn;
+  }
+  return generic ? generic->fn : nullptr;
+}
+
 // ------------------------------------------------------------ dispatch --
 using KernelFn = void (*)(const TiledArgs);
 
@@ -1233,6 +1426,16 @@ cudaError_t prepare_smem(KernelFn fn, uint32_t smem) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
   return e;
+}
+
+cudaError_t launch_rect(RectFn fn, const CUtensorMap& tmap, const TiledArgs& a, uint32_t blocks,
+                        uint32_t threads, uint32_t smem, cudaStream_t st, uint32_t beams) {
+  fn<<<dim3(blocks, beams), threads, smem, st>>>(tmap, a);
+  return cudaGetLastError();
+}
+
+cudaError_t prepare_rect(RectFn fn, uint32_t smem) {
+  return prepare_smem(reinterpret_cast<KernelFn>(fn), smem);
 }
 
 }  // namespace ddb

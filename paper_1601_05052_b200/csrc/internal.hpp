@@ -35,8 +35,17 @@ struct dd_context {
   uint32_t last_family = 0;
 };
 
+#include <cuda.h>
+
 struct dd_plan {
   dd_context* ctx = nullptr;
+  // rectangle family (DD_STAGING_RECT): kernel, group lows, tensor map cache
+  void (*rect_fn)(const CUtensorMap, const ddb::TiledArgs) = nullptr;
+  uint32_t* d_glo = nullptr;
+  CUtensorMap tmap{};
+  const float* tmap_in = nullptr;
+  uint64_t tmap_beam_stride = 0;
+  uint32_t tmap_beams = 0;
   uint32_t family = DD_STAGING_DIRECT;
   bool reference_order = false;
   ddb::TiledArgs args{};
@@ -70,6 +79,7 @@ cudaError_t launch_plan(const uint32_t* d_shifts, uint8_t* d_rec, uint2* d_ls, u
                         uint32_t tile_dm, uint32_t group, uint32_t rec_bytes, uint32_t window_format,
                         uint32_t* d_chan_span, cudaStream_t st);
 cudaError_t launch_max_u32(const uint32_t* d_v, uint64_t n, uint32_t* d_out, cudaStream_t st);
+cudaError_t launch_flush_read(const void* buf, uint64_t bytes, uint32_t* sink, cudaStream_t st);
 
 using KernelFn = void (*)(const TiledArgs);
 // Staged-kernel variant for work_dm x work_time; nullptr when not
@@ -98,6 +108,16 @@ cudaError_t launch_direct(const TiledArgs& a, uint32_t blocks, uint32_t threads,
 cudaError_t launch_smem(KernelFn fn, const TiledArgs& a, uint32_t blocks, uint32_t threads,
                         uint32_t smem, cudaStream_t st, uint32_t beams = 1);
 cudaError_t prepare_smem(KernelFn fn, uint32_t smem);
+// K6 rectangles (dedisp.cu) and their pre-pass (table.cu)
+using RectFn = void (*)(const CUtensorMap, const TiledArgs);
+RectFn find_rect_kernel(uint32_t k, uint32_t w, uint32_t items_time);
+cudaError_t launch_rect(RectFn fn, const CUtensorMap& tmap, const TiledArgs& a, uint32_t blocks,
+                        uint32_t threads, uint32_t smem, cudaStream_t st, uint32_t beams);
+cudaError_t prepare_rect(RectFn fn, uint32_t smem);
+cudaError_t launch_plan_rect(const uint32_t* d_shifts, uint32_t* d_glo, uint32_t* d_rec,
+                             uint32_t* d_max_width, uint32_t channels, uint32_t tiles_dm,
+                             uint32_t tile_dm, uint32_t rect_ch, uint32_t groups,
+                             uint32_t rec_words, cudaStream_t st);
 // checked builds (DDB_CHECKED): device bounds violations so far (dedisp.cu)
 cudaError_t debug_violations(unsigned long long* count, int* checked, int reset);
 

@@ -729,3 +729,69 @@ def test_live_plan_survives_a_smaller_plan_of_the_same_kernel(dev):
         p.execute(x.data_ptr(), out.data_ptr())
         dev.synchronize()
         assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
+
+
+@pytest.mark.parametrize("idx,cfg,flags", [
+    (5, K(96, 1, 1, 2), 4 << 8), (5, K(64, 1, 2, 2), 2 << 8), (5, K(128, 1, 1, 2), 0),
+    (0, K(32, 4, 1, 4), 0), (0, K(16, 8, 2, 4), 2 << 8), (0, K(32, 8, 1, 8), 0),
+])
+def test_rect_family_golden(dev, golden, idx, cfg, flags):
+    """K6 (staging "rect", one 3-D TMA box per channel group) on the golden
+    small-d instances: the whole output's fingerprint equals the
+    reference's, for full passes, channel-range passes and beams."""
+    import torch
+    g = golden["baseline"][idx]
+    setup, table, fb = _golden_instance(g)
+    d, s, c, t = g["num_dms"], setup.samples_per_second, setup.channels, g["num_samples"]
+    pitch = (t + 3) // 4 * 4
+    x = torch.zeros((c, pitch), device="cuda")
+    x[:, :t] = torch.from_numpy(fb.data).cuda()
+    sh = torch.from_numpy(table.shifts.view(np.int32)).cuda()
+    out = torch.full((d, s), float("nan"), device="cuda")
+    torch.cuda.synchronize()
+    p = dev.plan(sh.data_ptr(), c, d, s, t, pitch, cfg, 1, "rect",
+                 flags=flags | N.DD_CONFIG_GPU_TILING)
+    assert p.info()["family"] == "rect"
+    p.execute(x.data_ptr(), out.data_ptr())
+    dev.synchronize()
+    assert api.fingerprint(out.cpu()) == g["out_fnv"]
+    out.fill_(float("nan"))
+    for i, (c0, c1) in enumerate([(0, c // 3), (c // 3, c // 3 + 1), (c // 3 + 1, c)]):
+        if c1 > c0:
+            p.execute_channels(x.data_ptr(), out.data_ptr(), c0, c1, accumulate=i > 0)
+    dev.synchronize()
+    assert api.fingerprint(out.cpu()) == g["out_fnv"]
+    xb = torch.stack([x, x * 2.0])
+    ob = torch.full((2, d, s), float("nan"), device="cuda")
+    torch.cuda.synchronize()
+    p.execute_beams(2, xb.data_ptr(), c * pitch, ob.data_ptr(), d * s)
+    dev.synchronize()
+    assert api.fingerprint(ob[0].cpu()) == g["out_fnv"]
+    assert torch.equal(ob[1].view(torch.int32), (ob[0] * 2.0).view(torch.int32))
+
+
+def test_rect_family_non_monotone_table(dev):
+    """K6 assumes no ordering of the shifts (group lows by min scan): a
+    fault-injected table still reproduces the reference-order kernel."""
+    import torch
+    setup, d = api.APERTIF, 8
+    table = api.build_delay_table(setup, d)
+    sh_np = table.shifts.copy()
+    sh_np[3, ::5] = 0
+    sh_np[6, 10:40] += 9
+    t = api.instance_sizing(setup, d).num_samples
+    s, c = setup.samples_per_second, setup.channels
+    fb = api.noise_filterbank(setup, t, 1.0, 2)
+    x = torch.from_numpy(fb.data).cuda()
+    sh = torch.from_numpy(sh_np.view(np.int32)).cuda()
+    ref = torch.empty((d, s), device="cuda")
+    dev.plan(sh.data_ptr(), c, d, s, t, t).execute(x.data_ptr(), ref.data_ptr())
+    out = torch.full((d, s), float("nan"), device="cuda")
+    p = dev.plan(sh.data_ptr(), c, d, s, t, t, K(64, 2, 1, 4), 1, "rect",
+                 flags=N.DD_CONFIG_GPU_TILING)
+    p.execute(x.data_ptr(), out.data_ptr())
+    dev.synchronize()
+    assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
+    with pytest.raises(ValueError):  # spans beyond one TMA box: not this family
+        dev.plan(sh.data_ptr(), c, d, s, t, t, K(256, 1, 1, 8), 1, "rect",
+                 flags=N.DD_CONFIG_GPU_TILING | (1 << N.DD_CONFIG_CPS_SHIFT)).close()
