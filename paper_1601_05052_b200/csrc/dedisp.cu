@@ -1047,6 +1047,31 @@ __global__ void __launch_bounds__(160, 3) k_tmemwin_occ(const TiledArgs a) {
 // shared-memory operand per add, channels ascending, one fp32 accumulator
 // per output -- bit-exact).
 // ---------------------------------------------------------------------
+// K6 thread mapping: thread (it, id) owns times t0 + it + j*items_time
+// (j < W) and the K CONSECUTIVE DMs id*K .. id*K+K-1 of the tile, so its
+// per-channel offsets are one vector load (the output is mapping-invariant:
+// every output still sums its channels in order into one accumulator).
+template <int K>
+__device__ __forceinline__ void load_offsets(const uint32_t* o, uint32_t (&v)[K]) {
+  if constexpr (K % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < K; k += 4) {
+      const uint4 q = *reinterpret_cast<const uint4*>(o + k);
+      v[k] = q.x;
+      v[k + 1] = q.y;
+      v[k + 2] = q.z;
+      v[k + 3] = q.w;
+    }
+  } else if constexpr (K == 2) {
+    const uint2 q = *reinterpret_cast<const uint2*>(o);
+    v[0] = q.x;
+    v[1] = q.y;
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = o[k];
+  }
+}
+
 template <int K, int W, int IT>
 struct RectBody {
   const TiledArgs& a;
@@ -1063,28 +1088,25 @@ struct RectBody {
 #pragma unroll
       for (int j = 0; j < W; ++j) acc[k][j] = 0.0f;
   }
-  // row: this channel's rectangle row (sample t0 + lo_g at index 0);
-  // off: the channel's offsets (shift - lo_g) of the tile's DMs
+  // off: the channel's offsets (shift - lo_g) of the tile's DMs; row: this
+  // thread's first sample in the channel's rectangle row
   __device__ __forceinline__ void channel(const uint32_t* off, const float* row) {
-    row += it;
-    const float* p[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) p[k] = row + off[id + k * a.items_dm];
+    uint32_t o[K];
+    load_offsets<K>(off + id * K, o);
 #pragma unroll
     for (int n = 0; n + 1 < K * W; n += 2) {
       const int k0 = n / W, j0 = n % W, k1 = (n + 1) / W, j1 = (n + 1) % W;
       const float2 r = fadd2(make_float2(acc[k0][j0], acc[k1][j1]),
-                             make_float2(p[k0][j0 * stride()], p[k1][j1 * stride()]));
+                             make_float2(row[o[k0] + j0 * stride()], row[o[k1] + j1 * stride()]));
       acc[k0][j0] = r.x;
       acc[k1][j1] = r.y;
     }
-    if ((K * W) & 1) acc[K - 1][W - 1] += p[K - 1][(W - 1) * stride()];
+    if ((K * W) & 1) acc[K - 1][W - 1] += row[o[K - 1] + (W - 1) * stride()];
   }
   __device__ __forceinline__ void load(uint32_t dm0, uint32_t t0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const float* o =
-          beam_out(a) + static_cast<uint64_t>(dm0 + id + k * a.items_dm) * a.out_pitch + t0 + it;
+      const float* o = beam_out(a) + static_cast<uint64_t>(dm0 + id * K + k) * a.out_pitch + t0 + it;
 #pragma unroll
       for (int j = 0; j < W; ++j)
         acc[k][j] = t0 + it + j * stride() < a.s ? o[j * stride()] : 0.0f;
@@ -1093,9 +1115,8 @@ struct RectBody {
   __device__ __forceinline__ void store(uint32_t dm0, uint32_t t0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      DDB_CHECK(dm0 + id + k * a.items_dm < a.num_dms);
-      float* o =
-          beam_out(a) + static_cast<uint64_t>(dm0 + id + k * a.items_dm) * a.out_pitch + t0 + it;
+      DDB_CHECK(dm0 + id * K + k < a.num_dms);
+      float* o = beam_out(a) + static_cast<uint64_t>(dm0 + id * K + k) * a.out_pitch + t0 + it;
 #pragma unroll
       for (int j = 0; j < W; ++j)
         if (t0 + it + j * stride() < a.s) o[j * stride()] = acc[k][j];
@@ -1183,16 +1204,22 @@ __global__ void __launch_bounds__(1024 + 32) k_rect(const __grid_constant__ CUte
     const uint32_t c_lo = max(a.ch_begin, grp * a.rect_ch) - grp * a.rect_ch;
     const uint32_t c_hi = min(a.ch_end, (grp + 1) * a.rect_ch) - grp * a.rect_ch;
     if (active) {
+      // running pointers: the channel's offsets and this thread's first
+      // sample of the channel's rectangle row
+      const uint32_t* o = offs + c_lo * a.tile_dm;
+      const float* r = rows + c_lo * a.rect_w + body.it;
+      const uint32_t dof = a.tile_dm, drow = a.rect_w;
       uint32_t cc = c_lo;
       constexpr uint32_t U = K * W <= 8 ? 4 : 1;
       if constexpr (U > 1) {
         for (; cc + U <= c_hi; cc += U) {
 #pragma unroll
-          for (uint32_t u = 0; u < U; ++u)
-            body.channel(offs + (cc + u) * a.tile_dm, rows + (cc + u) * a.rect_w);
+          for (uint32_t u = 0; u < U; ++u) body.channel(o + u * dof, r + u * drow);
+          o += U * dof;
+          r += U * drow;
         }
       }
-      for (; cc < c_hi; ++cc) body.channel(offs + cc * a.tile_dm, rows + cc * a.rect_w);
+      for (; cc < c_hi; ++cc, o += dof, r += drow) body.channel(o, r);
     }
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot]);
@@ -1211,6 +1238,10 @@ static const RectVariant kRectVariants[] = {
     DDB_RV(1, 1, 0), DDB_RV(1, 2, 0), DDB_RV(1, 4, 0), DDB_RV(2, 1, 0), DDB_RV(2, 2, 0),
     DDB_RV(2, 4, 0), DDB_RV(4, 1, 0), DDB_RV(4, 2, 0), DDB_RV(4, 4, 0), DDB_RV(8, 1, 0),
     DDB_RV(8, 2, 0), DDB_RV(8, 4, 0), DDB_RV(16, 1, 0), DDB_RV(16, 2, 0),
+    // compile-time items_time (immediate strides) for the shapes small-d
+    // sweeps pick
+    DDB_RV(2, 1, 32), DDB_RV(2, 1, 64), DDB_RV(2, 1, 96), DDB_RV(2, 1, 128), DDB_RV(4, 1, 32),
+    DDB_RV(4, 1, 64), DDB_RV(2, 2, 64), DDB_RV(8, 1, 32), DDB_RV(4, 2, 32),
 };
 #undef DDB_RV
 

@@ -248,7 +248,7 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
         }
   // K6 rectangles for small trial counts, where a DM tile's delays span
   // few samples per channel group (the plan rejects wider spans: the
-  // tuner then skips the shape); GPU tiling, 32 or 64 channels per stage
+  // tuner then skips the shape); GPU tiling
   if (num_dms <= 128) {
     for (uint32_t it : {32u, 64u, 96u, 128u})
       for (uint32_t idm : {1u, 2u, 4u, 8u, 16u})
@@ -257,7 +257,9 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
             const uint64_t block = static_cast<uint64_t>(it) * idm;
             if (block < 32 || block > 512 || num_dms % (idm * wd) != 0) continue;
             if (find_rect_kernel(wd, wt, it) == nullptr) continue;
-            for (uint32_t cps : {2u, 4u}) {
+            // 32, 64 or 128 channels per TMA box (4 stages): wider boxes
+            // amortise the per-box cost (measured, small d)
+            for (uint32_t cps : {2u, 4u, 8u}) {
               dd_config c{it, idm, wt, wd, 1, DD_STAGING_RECT,
                           DD_CONFIG_GPU_TILING | (cps << DD_CONFIG_CPS_SHIFT)};
               v.push_back(c);

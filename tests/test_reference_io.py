@@ -76,7 +76,7 @@ def test_runs_are_recorded_in_new_documents():
     with the round-2 tuner (older committed sweeps predate it)."""
     docs = [json.load(open(p)) for p in glob.glob(os.path.join(ROOT, "tuning", "*_*.json"))
             if not p.endswith("_summary.json")]
-    fresh = [d for d in docs if d.get("environment", {}).get("l2") == "flushed"]
+    fresh = [d for d in docs if d.get("b200", {}).get("l2") == "flushed"]
     for d in fresh:
         assert all(len(r["runs_s"]) == d["repeats"] for r in d["records"])
 

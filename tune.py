@@ -29,13 +29,17 @@ sys.path.insert(0, ROOT)
 from paper_1601_05052_b200 import api  # noqa: E402
 
 
-def result_json(res: api.TuningResult, hbm_gbs: float, seconds: float) -> dict:
+def result_json(res: api.TuningResult, hbm_gbs: float, seconds: float, flush: bool = True) -> dict:
     d, s, c = res.num_dms, res.setup.samples_per_second, res.setup.channels
     doc = api.tuning_result_to_dict(res)
     best = res.best()
     roof = api.roofline_gflops(d, s, c, hbm_gbs)
     doc["b200"] = {"clock": "cuda events", "sweep_seconds": seconds, "hbm_gbs": hbm_gbs,
-                   "hbm_roofline_gflops": roof, "best_roofline_frac": best.gflops / roof}
+                   "hbm_roofline_gflops": roof, "best_roofline_frac": best.gflops / roof,
+                   "l2": "flushed" if flush else "warm",
+                   "l2_method": "before every timed run: a buffer twice the L2 written, then "
+                                "read back (clean lines), outside the CUDA events"
+                   if flush else "no flush between runs"}
     return doc
 
 
@@ -48,6 +52,7 @@ def main():
     p.add_argument("--max-configs", type=int, default=0)
     p.add_argument("--zero-dm", action="store_true")
     p.add_argument("--out", default=os.path.join(ROOT, "tuning"))
+    p.add_argument("--warm", action="store_true", help="no L2 flush between timed runs")
     a = p.parse_args()
     setup = api.find_builtin(a.setup)
     dms = a.dms or api.default_instances()
@@ -61,10 +66,10 @@ def main():
         t0 = time.time()
         fn = api.zero_dm_experiment if a.zero_dm else api.tune
         res = fn(setup, d, repeats=a.repeats, full_reference_space=a.space == "reference",
-                 max_configs=a.max_configs)
+                 max_configs=a.max_configs, flush_l2=not a.warm)
         dt = time.time() - t0
         results.append(res)
-        j = result_json(res, hbm, dt)
+        j = result_json(res, hbm, dt, not a.warm)
         name = f"{setup.name.lower()}_{d}{'_zerodm' if a.zero_dm else ''}.json"
         with open(os.path.join(a.out, name), "w") as f:
             json.dump(j, f, indent=1)
