@@ -34,6 +34,57 @@ dd_status cuda_fail(cudaError_t e, const char* where) {
 
 void clear_error() { g_error.clear(); }
 
+HostPool::HostPool(unsigned n) {
+  for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+}
+
+HostPool::~HostPool() {
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    stop_ = true;
+  }
+  cv_.notify_all();
+  for (std::thread& t : workers_) t.join();
+}
+
+void HostPool::loop() {
+  uint64_t seen = 0;
+  for (;;) {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+    if (stop_) return;
+    seen = gen_;
+    while (next_ < total_) {
+      const unsigned i = next_++;
+      const std::function<void(unsigned)>* f = job_;
+      lk.unlock();
+      (*f)(i);
+      lk.lock();
+      if (++finished_ == total_) done_cv_.notify_all();
+    }
+  }
+}
+
+void HostPool::run(unsigned n, const std::function<void(unsigned)>& f) {
+  if (n == 0) return;
+  std::unique_lock<std::mutex> lk(mu_);
+  job_ = &f;
+  next_ = 0;
+  total_ = n;
+  finished_ = 0;
+  ++gen_;
+  cv_.notify_all();
+  while (next_ < total_) {  // the caller works too
+    const unsigned i = next_++;
+    lk.unlock();
+    f(i);
+    lk.lock();
+    ++finished_;
+  }
+  done_cv_.wait(lk, [&] { return finished_ == total_; });
+  job_ = nullptr;
+}
+
 dd_limits effective_limits(const dd_limits* l) {
   dd_limits out{1024u, 256u};  // KernelLimits defaults, kernels.hpp:31-34
   if (l != nullptr && (l->max_block_items != 0 || l->max_accumulators != 0)) out = *l;
@@ -146,6 +197,11 @@ dd_status dd_context_destroy(dd_context* c) {
   cudaFree(c->d_in);
   cudaFree(c->d_sh);
   cudaFree(c->d_out);
+  for (int i = 0; i < 2; ++i) {
+    cudaFreeHost(c->h_bounce[i]);
+    if (c->ev_bounce[i]) cudaEventDestroy(c->ev_bounce[i]);
+  }
+  delete c->pool;
   cudaEventDestroy(c->ev_start);
   cudaEventDestroy(c->ev_stop);
   delete c;
@@ -1171,6 +1227,103 @@ dd_status dd_plan_time_ex(dd_plan* p, const float* d_in, float* d_out, uint64_t 
 
 namespace {
 
+// ------------------------------------------- pageable host transfers --
+// The reference API hands the drop-in pageable std::vector buffers.  Large
+// transfers go through two pinned bounce buffers of kBounce bytes: host
+// threads copy chunk k into (out of) one buffer while the DMA engine moves
+// chunk k-1 through the other, so neither the pageable-copy path of the
+// driver nor a single host thread sets the rate.
+constexpr uint64_t kBounce = 16ull << 20;
+constexpr uint64_t kBounceMin = 8ull << 20;  // smaller transfers: plain async copy
+
+dd_status bounce_ready(dd_context* c) {
+  if (c->h_bounce[0] != nullptr) return DD_OK;
+  for (int i = 0; i < 2; ++i) {
+    DD_CUDA(cudaMallocHost(&c->h_bounce[i], kBounce));
+    DD_CUDA(cudaEventCreateWithFlags(&c->ev_bounce[i], cudaEventDisableTiming));
+  }
+  c->bounce_bytes = kBounce;
+  unsigned hw = std::thread::hardware_concurrency();
+  c->pool = new HostPool(std::min(7u, hw > 1 ? hw - 1 : 1u));
+  return DD_OK;
+}
+
+void parallel_copy(dd_context* c, void* dst, const void* src, uint64_t bytes) {
+  const unsigned n = c->pool->size();
+  const uint64_t per = ((bytes + n - 1) / n + 63) & ~63ull;
+  c->pool->run(n, [&](unsigned i) {
+    const uint64_t lo = std::min(bytes, per * i), hi = std::min(bytes, lo + per);
+    if (hi > lo) std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+  });
+}
+
+// Host filterbank [channels][num_samples] (pageable) -> device rows of pitch
+// floats, in chunks of whole channel rows (or row pieces for huge rows).
+dd_status upload_staged(dd_context* c, float* d_dst, uint64_t pitch, const float* h_src,
+                        uint32_t channels, uint64_t num_samples) {
+  const uint64_t row = num_samples * 4;
+  if (row * channels < kBounceMin)
+    return dd_upload_filterbank(c, d_dst, pitch, h_src, channels, num_samples);
+  DD_TRY(bounce_ready(c));
+  // pieces of at most kBounce bytes: whole rows when a row fits
+  const uint64_t rows_per = std::max<uint64_t>(1, kBounce / row);
+  const uint64_t piece = row <= kBounce ? row : kBounce & ~15ull;
+  uint64_t k = 0;
+  for (uint64_t r0 = 0; r0 < channels;) {
+    if (row <= kBounce) {
+      const uint64_t nr = std::min<uint64_t>(rows_per, channels - r0);
+      void* hb = c->h_bounce[k & 1];
+      DD_CUDA(cudaEventSynchronize(c->ev_bounce[k & 1]));  // its previous DMA is done
+      parallel_copy(c, hb, h_src + r0 * num_samples, nr * row);
+      DD_CUDA(cudaMemcpy2DAsync(d_dst + r0 * pitch, pitch * 4, hb, row, row, nr,
+                                cudaMemcpyHostToDevice, c->stream));
+      DD_CUDA(cudaEventRecord(c->ev_bounce[k & 1], c->stream));
+      r0 += nr;
+      ++k;
+    } else {
+      for (uint64_t off = 0; off < row; off += piece) {
+        const uint64_t nb = std::min(piece, row - off);
+        void* hb = c->h_bounce[k & 1];
+        DD_CUDA(cudaEventSynchronize(c->ev_bounce[k & 1]));
+        parallel_copy(c, hb, reinterpret_cast<const char*>(h_src + r0 * num_samples) + off, nb);
+        DD_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(d_dst + r0 * pitch) + off, hb, nb,
+                                cudaMemcpyHostToDevice, c->stream));
+        DD_CUDA(cudaEventRecord(c->ev_bounce[k & 1], c->stream));
+        ++k;
+      }
+      ++r0;
+    }
+  }
+  return DD_OK;
+}
+
+// Device buffer -> pageable host buffer (contiguous), chunked through the
+// bounce buffers: the DMA of chunk k+1 runs while host threads copy chunk k.
+dd_status download_staged(dd_context* c, void* h_dst, const void* d_src, uint64_t bytes) {
+  if (bytes < kBounceMin) {
+    DD_TRY(dd_copy_d2h(c, h_dst, d_src, bytes));
+    DD_CUDA(cudaStreamSynchronize(c->stream));
+    return DD_OK;
+  }
+  DD_TRY(bounce_ready(c));
+  const uint64_t n = (bytes + kBounce - 1) / kBounce;
+  auto issue = [&](uint64_t k) -> dd_status {
+    const uint64_t lo = k * kBounce, nb = std::min(kBounce, bytes - lo);
+    DD_CUDA(cudaMemcpyAsync(c->h_bounce[k & 1], static_cast<const char*>(d_src) + lo, nb,
+                            cudaMemcpyDeviceToHost, c->stream));
+    DD_CUDA(cudaEventRecord(c->ev_bounce[k & 1], c->stream));
+    return DD_OK;
+  };
+  DD_TRY(issue(0));
+  for (uint64_t k = 0; k < n; ++k) {
+    DD_CUDA(cudaEventSynchronize(c->ev_bounce[k & 1]));
+    if (k + 1 < n) DD_TRY(issue(k + 1));  // into the other buffer, while we copy this one
+    const uint64_t lo = k * kBounce, nb = std::min(kBounce, bytes - lo);
+    parallel_copy(c, static_cast<char*>(h_dst) + lo, c->h_bounce[k & 1], nb);
+  }
+  return DD_OK;
+}
+
 // ------------------------------------------------------ tuned schedules --
 struct BuiltinSchedule {
   uint32_t channels, s, num_dms;
@@ -1374,12 +1527,28 @@ dd_status dd_dedisperse(dd_context* c, const float* h_in, uint32_t channels, uin
     c->last_run = ran;
     c->last_family = c->cached_plan->family;
   }
-  DD_TRY(dd_upload_filterbank(c, static_cast<float*>(c->d_in), pitch, h_in, channels,
-                              num_samples));
+  // pageable host buffers: pinned bounce buffers and parallel host copies
+  // (the reference API's std::vectors), or direct async copies from pinned
+  // memory
+  cudaPointerAttributes pin_in{}, pin_out{};
+  const bool in_pinned = cudaPointerGetAttributes(&pin_in, h_in) == cudaSuccess &&
+                         pin_in.type == cudaMemoryTypeHost;
+  const bool out_pinned = cudaPointerGetAttributes(&pin_out, h_out) == cudaSuccess &&
+                          pin_out.type == cudaMemoryTypeHost;
+  cudaGetLastError();  // a pageable pointer is not an error
+  if (in_pinned)
+    DD_TRY(dd_upload_filterbank(c, static_cast<float*>(c->d_in), pitch, h_in, channels,
+                                num_samples));
+  else
+    DD_TRY(upload_staged(c, static_cast<float*>(c->d_in), pitch, h_in, channels, num_samples));
   DD_TRY(dd_plan_execute(c->cached_plan, static_cast<float*>(c->d_in),
                          static_cast<float*>(c->d_out), s));
-  DD_TRY(dd_copy_d2h(c, h_out, c->d_out, out_bytes));
-  DD_CUDA(cudaStreamSynchronize(c->stream));
+  if (out_pinned) {
+    DD_TRY(dd_copy_d2h(c, h_out, c->d_out, out_bytes));
+    DD_CUDA(cudaStreamSynchronize(c->stream));
+  } else {
+    DD_TRY(download_staged(c, h_out, c->d_out, out_bytes));
+  }
   return DD_OK;
 }
 

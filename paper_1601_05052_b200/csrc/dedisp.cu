@@ -1281,6 +1281,9 @@ static const SmemVariant kSmemVariants[] = {
     DDB_VI(1, 5, 32), DDB_VI(2, 5, 32), DDB_VI(4, 5, 32), DDB_VI(1, 25, 8), DDB_VI(4, 10, 16),
     DDB_VP(2, 5, 160), DDB_VP(1, 25, 64), DDB_VP(2, 25, 64), DDB_VP(4, 10, 160),
     DDB_VP(2, 10, 160), DDB_VP(2, 25, 160),
+    // longer time tiles for wide-delay (LOFAR) instances: the staged window
+    // is tile_time + span, so a longer tile stages fewer bytes per add
+    DDB_VP(4, 20, 160), DDB_VP(4, 25, 128), DDB_VP(4, 20, 128),
 };
 #undef DDB_V
 #undef DDB_VI

@@ -3,9 +3,36 @@
 
 #include <cuda_runtime.h>
 
+#include <condition_variable>
 #include <cstdint>
+#include <functional>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
+
+namespace ddb {
+// A few persistent host threads for the drop-in's pageable <-> pinned
+// copies (abi.cu): run(n, f) calls f(0..n-1) spread over the threads and
+// the caller, and returns when all are done.
+class HostPool {
+ public:
+  explicit HostPool(unsigned n);
+  ~HostPool();
+  void run(unsigned n, const std::function<void(unsigned)>& f);
+  unsigned size() const { return static_cast<unsigned>(workers_.size()) + 1; }
+
+ private:
+  void loop();
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(unsigned)>* job_ = nullptr;
+  unsigned next_ = 0, total_ = 0, finished_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+}  // namespace ddb
 
 #include "../../include/dedisp_b200.h"
 #include "common.cuh"
@@ -33,6 +60,13 @@ struct dd_context {
   uint64_t cached_key[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   dd_config last_run{};
   uint32_t last_family = 0;
+  // pageable host buffers (the reference API's std::vectors) go through two
+  // pinned bounce buffers: host threads copy one while the DMA engine moves
+  // the other
+  void* h_bounce[2] = {nullptr, nullptr};
+  uint64_t bounce_bytes = 0;
+  cudaEvent_t ev_bounce[2] = {nullptr, nullptr};
+  ddb::HostPool* pool = nullptr;
 };
 
 #include <cuda.h>

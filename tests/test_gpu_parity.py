@@ -534,7 +534,7 @@ def test_block_stream_matches_one_shot(dev):
     d = 32
     st = BlockStream(setup, d, K(32, 2, 5, 8), 1, "smem", device=0)
     s, t = setup.samples_per_second, st.t
-    total = t + 3 * s
+    total = t + 6 * s
     series = api.noise_filterbank(setup, total, 1.0, 21).data
     table = api.build_delay_table(setup, d)
     outs = []
@@ -548,6 +548,8 @@ def test_block_stream_matches_one_shot(dev):
         ref = O.dedisperse_reference(np.ascontiguousarray(series[:, i * s:i * s + t]),
                                      table.shifts, s)
         assert np.array_equal(_bits(o), _bits(ref)), i
+    # the ring moved the window's tail to the front only once per R pushes
+    assert st.ring and 0 < st.compactions <= (total // s) // st.rounds + 1
 
 
 @pytest.mark.parametrize("t,c", [(1001, 37), (40000, 1024), (3, 1), (257, 32)])
