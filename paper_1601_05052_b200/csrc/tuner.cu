@@ -250,7 +250,17 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
   // few samples per channel group (the plan rejects wider spans: the
   // tuner then skips the shape); GPU tiling
   if (num_dms <= 128) {
-    for (uint32_t it : {32u, 64u, 96u, 128u})
+    // time tiles of 32..128 samples, plus tiles that deal the s samples out
+    // in k equal shares per SM (k = 1..4): an HBM-bound pass wants equal
+    // bytes per SM, not a ragged last wave
+    std::vector<uint32_t> its = {32u, 64u, 96u, 128u};
+    for (uint32_t k = 1; k <= 4; ++k) {
+      const uint32_t sms = static_cast<uint32_t>(std::max(1, ctx->sm_count));
+      const uint32_t it = ((s + sms * k - 1) / (sms * k) + 3u) & ~3u;
+      if (it >= 16 && it <= 256 && std::find(its.begin(), its.end(), it) == its.end())
+        its.push_back(it);
+    }
+    for (uint32_t it : its)
       for (uint32_t idm : {1u, 2u, 4u, 8u, 16u})
         for (uint32_t wt : {1u, 2u})
           for (uint32_t wd : {1u, 2u, 4u, 8u, 16u}) {

@@ -1,6 +1,9 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/final
 O=gpurun_out/final
+mkdir -p gpurun_out/tuning_small
+timeout 600 python tune.py --setup Apertif --dms 2 --dms 4 --dms 8 --dms 16 --dms 32 --out gpurun_out/tuning_small > $O/tune_small.log 2>&1
+tail -6 $O/tune_small.log
 timeout 1200 python -m pytest tests -m gpu -q > $O/gputest.log 2>&1
 tail -3 $O/gputest.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
