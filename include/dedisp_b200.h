@@ -338,6 +338,26 @@ dd_status dd_debug_violations(uint64_t* count, int* checked, int reset);
  * the reference's without keeping the reference's output around. */
 dd_status dd_fingerprint(const void* data, uint64_t bytes, uint64_t* out);
 
+/* ---------------------------------------------- streaming blocks ----- */
+/* Consecutive seconds of a live observation (the
+ * reference handles one padded block, setup.cpp:130-133).  The stream keeps
+ * a device ring of the last t = instance_sizing(setup, num_dms).num_samples
+ * samples per channel; every push appends one second (host [channels][s],
+ * channel-major) and, once the window is full, dedisperses its first second:
+ * h_out (num_dms x s, may be NULL) receives exactly what a one-shot pass over
+ * the same t samples gives, *produced = 1.  cfg == NULL (or AUTO without
+ * flags) runs the instance's tuned schedule.  Synchronous per push. */
+typedef struct dd_block_stream dd_block_stream;
+dd_status dd_block_stream_create(dd_context* ctx, const dd_setup* setup, uint32_t num_dms,
+                                 const dd_config* cfg, dd_block_stream** out);
+dd_status dd_block_stream_push(dd_block_stream* stream, const float* h_second, float* h_out,
+                               int* produced);
+/* counters and the device output of the last pass (any may be NULL) */
+dd_status dd_block_stream_info(const dd_block_stream* stream, uint64_t* num_samples,
+                               uint64_t* pushes, uint64_t* outputs, uint64_t* compactions,
+                               const float** d_out);
+dd_status dd_block_stream_destroy(dd_block_stream* stream);
+
 /* ---------------------------------------------- synthetic input ------- */
 /* noise_filterbank, filterbank.cpp:60-80: mt19937_64(seed), Box-Muller,
  * channel-major fill, float(sigma * g).  Host memory; threads = 0 -> all. */

@@ -132,6 +132,11 @@ SIGNATURES = {
     "dd_schedule_set": (i32, [u32, u32, u32, C.POINTER(dd_config)]),
     "dd_schedule_get": (i32, [u32, u32, u32, C.POINTER(dd_config), C.POINTER(C.c_int)]),
     "dd_last_run_config": (i32, [P, C.POINTER(dd_config), pu32]),
+    "dd_block_stream_create": (i32, [P, C.POINTER(dd_setup), u32, C.POINTER(dd_config),
+                                     C.POINTER(P)]),
+    "dd_block_stream_push": (i32, [P, P, P, C.POINTER(C.c_int)]),
+    "dd_block_stream_info": (i32, [P, pu64, pu64, pu64, pu64, C.POINTER(P)]),
+    "dd_block_stream_destroy": (i32, [P]),
     "dd_plan_execute_channels": (i32, [P, P, P, u64, u32, u32, C.c_int]),
     "dd_plan_execute_beams": (i32, [P, u32, P, u64, P, u64, u64]),
     "dd_dedisperse_device": (i32, [P, P, u32, u64, u64, P, u32, u32, C.POINTER(dd_config),

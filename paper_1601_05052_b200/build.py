@@ -20,7 +20,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdedisp_b200.so")
 LIB_CHECKED = os.path.join(PKG, "libdedisp_b200_checked.so")
-SOURCES = ["table.cu", "dedisp.cu", "abi.cu", "tuner.cu", "ingest.cu", "host.cpp"]
+SOURCES = ["table.cu", "dedisp.cu", "abi.cu", "tuner.cu", "ingest.cu", "stream.cu", "host.cpp"]
 HEADERS = ["common.cuh", "internal.hpp", "regwin_dispatch.cuh", "schedules.inc"]
 PUBLIC = [os.path.join(ROOT, "include", "dedisp_b200.h"),
           os.path.join(ROOT, "include", "dedisp", "b200.hpp")]

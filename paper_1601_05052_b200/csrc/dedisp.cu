@@ -118,6 +118,19 @@ __device__ __forceinline__ float* beam_out(const TiledArgs& a) {
   return a.out + blockIdx.y * a.out_beam_stride;
 }
 
+// Consumers waiting for a stage: spin on try_wait, or (DDB_CONSUMER_SLEEP,
+// an A/B switch) let the hardware park the warp until the phase completes so
+// the spin does not take issue slots from the warps that have work.
+#ifndef DDB_CONSUMER_SLEEP
+#define DDB_CONSUMER_SLEEP 0
+#endif
+__device__ __forceinline__ void consumer_wait(uint64_t* bar, uint32_t parity) {
+  if constexpr (DDB_CONSUMER_SLEEP)
+    mbar_wait_sleep(bar, parity);
+  else
+    mbar_wait(bar, parity);
+}
+
 struct Pipe {
   uint64_t* full;   // [nstage] data landed (TMA transaction count)
   uint64_t* empty;  // [nstage] every consumer warp is done with the slot
@@ -322,7 +335,7 @@ __device__ __forceinline__ void staged_loop_with(const TiledArgs& a, uint8_t* sm
         body.zero();
     }
     const uint32_t slot = g % a.nstage;
-    mbar_wait(&p.full[slot], (g / a.nstage) & 1u);
+    consumer_wait(&p.full[slot], (g / a.nstage) & 1u);
     uint32_t ch0, ncs;
     stage_channels<PK>(a, q, ch0, ncs);
     const uint8_t* rbase = p.recs + slot * a.cps * a.rec_bytes;
@@ -1192,7 +1205,7 @@ __global__ void __launch_bounds__(1024 + 32) k_rect(const __grid_constant__ CUte
       else
         body.zero();
     }
-    mbar_wait(&full[slot], (g / a.nstage) & 1u);
+    consumer_wait(&full[slot], (g / a.nstage) & 1u);
     const uint8_t* st = stages + slot * stage_bytes;
     const uint32_t grp0 = g_begin + q;
     const float* rows = reinterpret_cast<const float*>(st) +

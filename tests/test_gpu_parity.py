@@ -797,3 +797,42 @@ def test_rect_family_non_monotone_table(dev):
     with pytest.raises(ValueError):  # spans beyond one TMA box: not this family
         dev.plan(sh.data_ptr(), c, d, s, t, t, K(256, 1, 1, 8), 1, "rect",
                  flags=N.DD_CONFIG_GPU_TILING | (1 << N.DD_CONFIG_CPS_SHIFT)).close()
+
+
+@pytest.mark.parametrize("rate,cfg", [(320, None), (322, K(32, 2, 5, 8))])
+def test_c_abi_block_stream(dev, rate, cfg):
+    """dd_block_stream_*: the streaming-ingest entry point of the C-ABI.  Each
+    pushed second yields, once the window is full, exactly the one-shot
+    pass over the same samples (checked against the oracle); with s % 4 != 0
+    the window is compacted through a temporary on every slide."""
+    import ctypes as C
+    setup = api.ObservationSetup("strm", rate, 24, 300.0, 1.0, 0.0, 0.5)
+    d, s = 32, rate
+    h = C.c_void_p()
+    kc = None
+    if cfg is not None:
+        kc = N.dd_config(cfg.items_time, cfg.items_dm, cfg.work_time, cfg.work_dm, 1,
+                         N.STAGING["smem"], N.DD_CONFIG_GPU_TILING)
+    N.check(N.lib().dd_block_stream_create(dev.handle, C.byref(setup.c()), d,
+                                           C.byref(kc) if kc is not None else None, C.byref(h)))
+    t = api.instance_sizing(setup, d).num_samples
+    total = t + 6 * s
+    series = api.noise_filterbank(setup, total, 1.0, 23).data
+    table = api.build_delay_table(setup, d)
+    out = np.empty((d, s), np.float32)
+    produced, got = C.c_int(), []
+    for n in range(total // s):
+        sec = np.ascontiguousarray(series[:, n * s:(n + 1) * s])
+        N.check(N.lib().dd_block_stream_push(h, sec.ctypes.data, out.ctypes.data,
+                                             C.byref(produced)))
+        if produced.value:
+            got.append(out.copy())
+    assert len(got) == (total - t) // s + 1
+    for i, o in enumerate(got):
+        ref = O.dedisperse_reference(np.ascontiguousarray(series[:, i * s:i * s + t]),
+                                     table.shifts, s)
+        assert np.array_equal(_bits(o), _bits(ref)), i
+    comp = C.c_uint64()
+    N.check(N.lib().dd_block_stream_info(h, None, None, None, C.byref(comp), None))
+    assert comp.value >= 1
+    N.check(N.lib().dd_block_stream_destroy(h))
