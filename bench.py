@@ -55,7 +55,7 @@ def parse():
     p.add_argument("--flush-mb", type=int, default=256)
     p.add_argument("--e2e-chunks", type=int, default=8)
     p.add_argument("--e2e-channel-groups", type=int, default=2)
-    p.add_argument("--e2e-h2d", default="auto", choices=["auto", "time", "channels"])
+    p.add_argument("--e2e-h2d", default="auto", choices=["auto", "time", "channels", "sharded"])
     p.add_argument("--e2e-single", action="store_true",
                    help="e2e over isolated blocks instead of a double-buffered stream")
     p.add_argument("--plumbing-check", action="store_true",

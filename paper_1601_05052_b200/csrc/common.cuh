@@ -123,6 +123,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int32_t
       : "memory");
 }
 
+// L2 prefetch of a 3-D TMA tile (no shared memory, no completion): lets a
+// producer reach further ahead into HBM than its shared-memory stages hold.
+__device__ __forceinline__ void tma_prefetch_3d(const void* tmap, int32_t c0, int32_t c1,
+                                                int32_t c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(tmap),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
 // Two IEEE round-to-nearest fp32 adds in one instruction (SASS: FADD2).
 // Each lane is an independent correctly-rounded add, so the per-output
 // accumulation order (and hence bit-exactness) is unchanged.

@@ -1137,6 +1137,10 @@ struct RectBody {
   }
 };
 
+#ifndef DDB_RECT_PREFETCH
+#define DDB_RECT_PREFETCH 0
+#endif
+
 template <int K, int W, int IT>
 __global__ void __launch_bounds__(1024 + 32) k_rect(const __grid_constant__ CUtensorMap tmap,
                                                     const TiledArgs a) {
@@ -1187,6 +1191,17 @@ __global__ void __launch_bounds__(1024 + 32) k_rect(const __grid_constant__ CUte
       mbar_expect_tx(bar, box_bytes + a.rec_bytes);
       tma_load_3d(st, &tmap, x0, static_cast<int32_t>(grp * a.rect_ch),
                   static_cast<int32_t>(blockIdx.y), bar);
+      if constexpr (DDB_RECT_PREFETCH > 0) {
+        // warm L2 with the box DDB_RECT_PREFETCH chunks ahead
+        const uint32_t gp = g + DDB_RECT_PREFETCH;
+        if (gp < total) {
+          const uint32_t bp = b_first + gp / nchunk, grpp = g_begin + gp % nchunk;
+          const int32_t xp =
+              static_cast<int32_t>((t0 + __ldg(a.glo + bp * a.rect_groups + grpp)) & ~3u);
+          tma_prefetch_3d(&tmap, xp, static_cast<int32_t>(grpp * a.rect_ch),
+                          static_cast<int32_t>(blockIdx.y));
+        }
+      }
       bulk_g2s(st + ((box_bytes + 127u) & ~127u),
                a.rec + (static_cast<uint64_t>(b) * a.rect_groups + grp) * a.rec_bytes, a.rec_bytes,
                bar);

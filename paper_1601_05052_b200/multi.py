@@ -216,8 +216,11 @@ class ShardedDedisperser:
             h2d = "time" if self.world == 1 else "sharded"
         if self.world > 1 and h2d in ("time", "channels"):
             h2d = "sharded"
-        if self.world == 1 and h2d in ("sharded", "broadcast"):
+        if self.world == 1 and h2d == "broadcast":
             h2d = "time"
+        # (h2d="sharded" on one rank runs the N-rank route with N = 1 -- the
+        # channel-group uploads, per-group events and accumulating kernels,
+        # with the all-gather a no-op: how tests exercise it on one GPU)
         groups = []
         if h2d == "sharded":
             groups = channel_groups(c, self.world, channel_groups_ if staged else 1)

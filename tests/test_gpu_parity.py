@@ -836,3 +836,31 @@ def test_c_abi_block_stream(dev, rate, cfg):
     N.check(N.lib().dd_block_stream_info(h, None, None, None, C.byref(comp), None))
     assert comp.value >= 1
     N.check(N.lib().dd_block_stream_destroy(h))
+
+
+def test_sharded_route_on_one_rank(dev, golden):
+    """The N-rank e2e route (each rank's channel-group share H2D, the
+    per-group all-gather -- a no-op at N = 1 --, kernels accumulating group by
+    group, per-chunk D2H) run on one GPU: one block and a double-buffered
+    stream, whole outputs against the reference's fingerprint."""
+    import torch
+    from paper_1601_05052_b200 import multi
+    g = golden["baseline"][0]
+    setup, table, fb = _golden_instance(g)
+    dd = multi.ShardedDedisperser(setup, g["num_dms"], K(32, 4, 12, 8), 1, "tmem", device=0,
+                                  gpu_tiling=True, stage_channels=15)
+    dd.pipeline(4, 4, h2d="sharded")
+    assert dd.h2d_mode == "sharded" and len(dd.groups) == 4
+    assert dd.h2d_bytes() == setup.channels * dd.num_samples * 4
+    host = torch.from_numpy(fb.data).pin_memory()
+    out = torch.full((dd.count, setup.samples_per_second), float("nan")).pin_memory()
+    dd.run_host(host, out)
+    torch.cuda.synchronize()
+    assert O.fnv1a(out.numpy()) == g["out_fnv"]
+    host2 = (host * 2).pin_memory()
+    outs = [torch.full_like(out, float("nan")).pin_memory() for _ in range(2)]
+    dd.stream_host([host, host2], outs, 5)
+    torch.cuda.synchronize()
+    assert O.fnv1a(outs[0].numpy()) == g["out_fnv"]  # block 4 = host
+    ref = out.numpy()
+    assert np.array_equal(_bits(outs[1].numpy()), _bits(ref * 2))  # block 3 = host2
