@@ -240,3 +240,48 @@ def test_cxx_analysis_layer(tmp_path):
     assert r.returncode == 0, r.stderr
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "analysis: ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_tuned_schedules_follow_the_committed_sweeps():
+    """The built-in schedules (csrc/schedules.inc, the one-shot entry points'
+    AUTO) are the tuner's picks in tuning/*.json; a registered schedule takes
+    precedence and can be forgotten; an invalid one is rejected."""
+    import glob
+    import json
+    n = 0
+    for path in glob.glob(os.path.join(ROOT, "tuning", "*_*.json")):
+        if path.endswith("_summary.json"):
+            continue
+        doc = json.load(open(path))
+        best = doc["records"][doc["best_index"]]
+        s = doc["setup"]
+        got = api.schedule_get(s["channels"], s["samples_per_second"], doc["num_dms"])
+        assert got is not None, path
+        cfg, depth, staging, flags, builtin = got
+        assert builtin
+        assert (cfg.items_time, cfg.items_dm, cfg.work_time, cfg.work_dm) == \
+            (best["items_time"], best["items_dm"], best["work_time"], best["work_dm"]), path
+        assert (depth, staging, flags) == (best["b200"]["dm_tile_depth"], best["b200"]["staging"],
+                                           best["b200"]["flags"]), path
+        n += 1
+    assert n >= 24
+    assert api.schedule_get(7, 100, 3) is None
+    rec = api.TuningRecord(api.KernelConfig(16, 2, 5, 2), staging="smem",
+                           flags=8 << N.DD_CONFIG_CPS_SHIFT)
+    api.schedule_set(7, 160, 4, rec)
+    cfg, depth, staging, flags, builtin = api.schedule_get(7, 160, 4)
+    assert (cfg, staging, flags, builtin) == (rec.config, "smem", rec.flags, False)
+    api.schedule_set(7, 160, 4, None)
+    assert api.schedule_get(7, 160, 4) is None
+    with pytest.raises(ValueError):  # tile_dm 4 does not divide 6 trials
+        api.schedule_set(7, 160, 6, rec)
+
+
+def test_fingerprint_matches_the_fixture_hash():
+    """dd_fingerprint (the bench's parity check) is the FNV-1a 64 the golden
+    fixtures use (the oracle's hash), on arbitrary bytes."""
+    rng = np.random.default_rng(3)
+    for n in (0, 1, 7, 4096, 100003):
+        a = rng.integers(0, 256, size=n, dtype=np.uint8)
+        assert api.fingerprint(a) == O.fnv1a(a)
+    assert api.fingerprint(np.zeros(0, np.uint8)) == "cbf29ce484222325"
