@@ -723,6 +723,20 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* r) {
       : "memory");
 }
 
+// W = 12 as x8 + x4 in ONE asm statement: both loads address the same
+// register ([taddr], [taddr+8]), so ptxas moves the column to a uniform
+// register once (one R2UR per DM instead of two)
+__device__ __forceinline__ void tmem_ld12(uint32_t taddr, float* r) {
+  asm volatile(
+      "{\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%12];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%8, %9, %10, %11}, [%12+8];\n\t}"
+      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]),
+        "=f"(r[7]), "=f"(r[8]), "=f"(r[9]), "=f"(r[10]), "=f"(r[11])
+      : "r"(taddr)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
                : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3])
@@ -742,6 +756,9 @@ __device__ __forceinline__ void tmem_wait_ld() {
 #endif
 #ifndef DDB_TMEM_READ16
 #define DDB_TMEM_READ16 0
+#endif
+#ifndef DDB_TMEM_LD12
+#define DDB_TMEM_LD12 1
 #endif
 // launch bound of k_tmemwin: 288 threads (up to 8 consumer warps), or an A/B
 // build bounded to 160 threads x 2 CTAs (<= 204 registers)
@@ -911,6 +928,8 @@ struct TmemBody {
           const uint32_t c = taddr + off[k + h];
           if constexpr (kRead16) {
             tmem_ld16(c, v[h]);
+          } else if constexpr (W == 12 && DDB_TMEM_LD12) {
+            tmem_ld12(c, v[h]);
           } else {
 #pragma unroll
             for (int j = 0; j + 8 <= W; j += 8) tmem_ld8(c + j, &v[h][j]);
