@@ -737,6 +737,20 @@ __device__ __forceinline__ void tmem_ld12(uint32_t taddr, float* r) {
       : "memory");
 }
 
+// W = 20 as x16 + x4 in one asm statement (two LDTMs instead of three)
+__device__ __forceinline__ void tmem_ld20(uint32_t taddr, float* r) {
+  asm volatile(
+      "{\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%20];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%16, %17, %18, %19}, [%20+16];\n\t}"
+      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]),
+        "=f"(r[7]), "=f"(r[8]), "=f"(r[9]), "=f"(r[10]), "=f"(r[11]), "=f"(r[12]), "=f"(r[13]),
+        "=f"(r[14]), "=f"(r[15]), "=f"(r[16]), "=f"(r[17]), "=f"(r[18]), "=f"(r[19])
+      : "r"(taddr)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
                : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3])
@@ -759,6 +773,9 @@ __device__ __forceinline__ void tmem_wait_ld() {
 #endif
 #ifndef DDB_TMEM_LD12
 #define DDB_TMEM_LD12 1
+#endif
+#ifndef DDB_TMEM_LD20
+#define DDB_TMEM_LD20 0
 #endif
 // launch bound of k_tmemwin: 288 threads (up to 8 consumer warps), or an A/B
 // build bounded to 160 threads x 2 CTAs (<= 204 registers)
@@ -930,6 +947,8 @@ struct TmemBody {
             tmem_ld16(c, v[h]);
           } else if constexpr (W == 12 && DDB_TMEM_LD12) {
             tmem_ld12(c, v[h]);
+          } else if constexpr (W == 20 && DDB_TMEM_LD20) {
+            tmem_ld20(c, v[h]);
           } else {
 #pragma unroll
             for (int j = 0; j + 8 <= W; j += 8) tmem_ld8(c + j, &v[h][j]);
