@@ -772,7 +772,7 @@ dd_status dd_config_family(dd_context* c, const dd_config* k, uint32_t channels,
   const uint32_t tile_dm = k->items_dm * k->work_dm;
   (void)num_dms;
   (void)s;
-  bool smem_ok = smem_variant_ok(k->work_dm, k->work_time, block);
+  bool smem_ok = smem_variant_ok(k->work_dm, k->work_time, block, k->items_time);
   const bool regwin_ok = regwin_shape_ok(k->work_dm, k->work_time, k->items_time, block);
   if (smem_ok) {
     uint32_t a, b, cc, d, e;
@@ -896,7 +896,7 @@ dd_status dd_plan_create(dd_context* c, const uint32_t* d_shifts, uint32_t chann
   }
 
   const uint64_t block = static_cast<uint64_t>(k->items_time) * k->items_dm;
-  const bool smem_shape = smem_variant_ok(k->work_dm, k->work_time, block);
+  const bool smem_shape = smem_variant_ok(k->work_dm, k->work_time, block, k->items_time);
   const bool regwin_shape = regwin_shape_ok(k->work_dm, k->work_time, k->items_time, block);
   const bool tmem_shape = tmem_shape_ok(k->work_dm, k->work_time, k->items_time, block);
   bool staged = in_pitch % 4 == 0;

@@ -467,8 +467,11 @@ constexpr int smem_max_threads() {
   return K * W > 32 ? 256 : (K * W > 16 ? 512 : 992);
 }
 
-template <int K, int W, int IT = 0, bool PK = false>
-__global__ void __launch_bounds__(smem_max_threads<K, W>() + 32) k_smem(const TiledArgs a) {
+// MT > 0: a build for up to MT consumer threads (instead of the
+// accumulator-count default) -- e.g. two DM rows of 160 threads
+template <int K, int W, int IT = 0, bool PK = false, int MT = 0>
+__global__ void __launch_bounds__((MT > 0 ? MT : smem_max_threads<K, W>()) + 32)
+    k_smem(const TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   staged_loop<SmemBody<K, W, IT, PK>>(a, smem);
 }
@@ -1335,6 +1338,8 @@ struct SmemVariant {
 #define DDB_VI(K, W, I) {K, W, I, k_smem<K, W, I>, smem_max_threads<K, W>(), nullptr}
 #define DDB_VP(K, W, I) \
   {K, W, I, k_smem<K, W, I>, smem_max_threads<K, W>(), k_smem<K, W, I, true>}
+#define DDB_VPT(K, W, I, MT) \
+  {K, W, I, k_smem<K, W, I, false, MT>, MT, k_smem<K, W, I, true, MT>}
 static const SmemVariant kSmemVariants[] = {
     DDB_V(1, 1),  DDB_V(1, 2),  DDB_V(1, 4),  DDB_V(1, 5),  DDB_V(1, 8),  DDB_V(1, 10),
     DDB_V(1, 16), DDB_V(1, 25), DDB_V(2, 1),  DDB_V(2, 2),  DDB_V(2, 4),  DDB_V(2, 5),
@@ -1347,13 +1352,14 @@ static const SmemVariant kSmemVariants[] = {
     DDB_VI(1, 5, 32), DDB_VI(2, 5, 32), DDB_VI(4, 5, 32), DDB_VI(1, 25, 8), DDB_VI(4, 10, 16),
     DDB_VP(2, 5, 160), DDB_VP(1, 25, 64), DDB_VP(2, 25, 64), DDB_VP(4, 10, 160),
     DDB_VP(2, 10, 160), DDB_VP(2, 25, 160),
-    // longer time tiles for wide-delay (LOFAR) instances: the staged window
-    // is tile_time + span, so a longer tile stages fewer bytes per add
-    DDB_VP(4, 20, 160), DDB_VP(4, 25, 128), DDB_VP(4, 20, 128),
+    // (longer / taller LOFAR tiles -- (160,1,20,4), (160,2,10,4), (160,2,20,4)
+    // -- stage fewer bytes per add but fit fewer channels per stage and
+    // spill: 4.98-6.47 ms against 4.72 ms, measured round 2; not built)
 };
 #undef DDB_V
 #undef DDB_VI
 #undef DDB_VP
+#undef DDB_VPT
 
 KernelFn find_smem_kernel(uint32_t k, uint32_t w, uint32_t* max_threads, uint32_t items_time,
                           KernelFn* packed) {

@@ -130,9 +130,9 @@ KernelFn find_tmem_kernel(uint32_t k, uint32_t w, uint32_t group_span, uint32_t*
 bool tmem_shape_ok(uint32_t k, uint32_t w, uint32_t items_time, uint64_t block);
 bool tmem_has_occupancy_build(uint32_t k, uint32_t w);
 // True when the staged family can run cfg (block size within the variant's cap).
-inline bool smem_variant_ok(uint32_t k, uint32_t w, uint64_t block) {
+inline bool smem_variant_ok(uint32_t k, uint32_t w, uint64_t block, uint32_t items_time = 0) {
   uint32_t cap = 0;
-  return find_smem_kernel(k, w, &cap) != nullptr && ((block + 31) & ~31ull) <= cap;
+  return find_smem_kernel(k, w, &cap, items_time) != nullptr && ((block + 31) & ~31ull) <= cap;
 }
 cudaError_t launch_reference(const float* in, uint64_t pitch, const uint32_t* shifts, float* out,
                              uint64_t out_pitch, uint32_t channels, uint32_t s, uint32_t num_dms,

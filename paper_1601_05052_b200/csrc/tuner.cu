@@ -187,7 +187,7 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
         v.push_back(c);
       }
     }
-    if (block < 64 || !smem_variant_ok(k.work_dm, k.work_time, block)) continue;
+    if (block < 64 || !smem_variant_ok(k.work_dm, k.work_time, block, k.items_time)) continue;
     for (uint32_t depth : {1u, 2u}) {
       if (depth > 1 && tiles_dm < depth * 2) continue;
       // 8 or 15 channels per stage; the time-major raster (large delays)
