@@ -697,6 +697,12 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
                : "memory");
 }
 
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+               "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3])
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
@@ -779,6 +785,9 @@ __device__ __forceinline__ void tmem_wait_ld() {
 #endif
 #ifndef DDB_TMEM_LD20
 #define DDB_TMEM_LD20 0
+#endif
+#ifndef DDB_TMEM_ST_SPLIT
+#define DDB_TMEM_ST_SPLIT 1
 #endif
 // launch bound of k_tmemwin: 288 threads (up to 8 consumer warps), or an A/B
 // build bounded to 160 threads x 2 CTAs (<= 204 registers)
@@ -903,7 +912,20 @@ struct TmemBody {
   __device__ __forceinline__ void commit(Pre& n, uint32_t buf = 0) const {
     if (n.nv == 0) return;
     const uint32_t taddr = this->taddr + buf;
-    tmem_st32(taddr, n.win);
+    if constexpr (DDB_TMEM_ST_SPLIT == 1) {
+      // four x8 stores: each can issue as soon as its two 16-byte loads
+      // have landed instead of one x32 store waiting for all eight
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tmem_st8(taddr + 8 * q, n.win + 8 * q);
+    } else if constexpr (DDB_TMEM_ST_SPLIT == 2) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) tmem_st4(taddr + 4 * q, n.win + 4 * q);
+    } else if constexpr (DDB_TMEM_ST_SPLIT == 3) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) tmem_st16(taddr + 16 * q, n.win + 16 * q);
+    } else {
+      tmem_st32(taddr, n.win);
+    }
     if constexpr (kTail > 0) {
       // columns 32.. of the widest window (alignment + SPAN + W): an x8,
       // x16 or x32 store sized at compile time keeps the extra live
