@@ -789,6 +789,9 @@ __device__ __forceinline__ void tmem_wait_ld() {
 #ifndef DDB_TMEM_ST_SPLIT
 #define DDB_TMEM_ST_SPLIT 1
 #endif
+#ifndef DDB_TMEM_TAIL_EARLY
+#define DDB_TMEM_TAIL_EARLY 1
+#endif
 // launch bound of k_tmemwin: 288 threads (up to 8 consumer warps), or an A/B
 // build bounded to 160 threads x 2 CTAs (<= 204 registers)
 #ifndef DDB_TMEM_LB2
@@ -820,6 +823,9 @@ struct TmemBody {
   // window columns beyond the first 32: 0, 8, 16 or 32
   static constexpr int kNeed = W + SPAN + 3 - 32;
   static constexpr int kTail = kNeed <= 0 ? 0 : kNeed <= 8 ? 8 : kNeed <= 16 ? 16 : 32;
+  // an x8 tail loaded right after the head (DDB_TMEM_TAIL_EARLY), so its
+  // shared-memory latency overlaps the head's stores
+  static constexpr bool kTailEarly = DDB_TMEM_TAIL_EARLY && kTail == 8;
   static_assert(kTail == 0 || COLS == 64, "windows past 32 columns need 64 per warp");
   const TiledArgs& a;
   uint32_t col, dml, taddr;
@@ -846,6 +852,7 @@ struct TmemBody {
     uint32_t nv;      // 16-byte window vectors to stage; 0 = slow path
     const float* base;  // this lane's 16-byte aligned window start
     float win[32];  // first 32 window columns (fast path)
+    float tail[kTailEarly ? 8 : 1];  // columns 32..39, loaded with the head
   };
 
   // Offsets + (fast) the first half of the window: only the 16-byte vectors
@@ -906,6 +913,15 @@ struct TmemBody {
         lds128_maybe(static_cast<uint32_t>(i) < n.nv, pa + 4 * i, n.win[4 * i],
                      n.win[4 * i + 1], n.win[4 * i + 2], n.win[4 * i + 3]);
     }
+    if constexpr (kTailEarly) {
+#ifdef DDB_CHECKED
+      if (n.nv > 8) chk.check(pa + 32, 4 * static_cast<int>(min(n.nv - 8u, 2u)));
+#endif
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        lds128_maybe(n.nv > 8u + i, pa + 32 + 4 * i, n.tail[4 * i], n.tail[4 * i + 1],
+                     n.tail[4 * i + 2], n.tail[4 * i + 3]);
+    }
   }
 
   // Window -> this lane's TMEM row; afterwards n.win may be refilled.
@@ -926,7 +942,9 @@ struct TmemBody {
     } else {
       tmem_st32(taddr, n.win);
     }
-    if constexpr (kTail > 0) {
+    if constexpr (kTailEarly) {
+      if (n.nv > 8) tmem_st8(taddr + 32, n.tail);
+    } else if constexpr (kTail > 0) {
       // columns 32.. of the widest window (alignment + SPAN + W): an x8,
       // x16 or x32 store sized at compile time keeps the extra live
       // registers to what the variant can need
