@@ -108,6 +108,10 @@ typedef struct dd_config {
  * synchronisation, smaller ones leave shared memory for more CTAs per SM. */
 #define DD_CONFIG_CPS_SHIFT 8u
 #define DD_CONFIG_CPS_MASK (0xfu << DD_CONFIG_CPS_SHIFT)
+/* Fixed-slot staged families: twice the DD_CONFIG_CPS channels per stage
+ * (up to 30; stages that wide amortise the per-stage synchronisation
+ * further where shared memory allows). */
+#define DD_CONFIG_WIDE_STAGES 0x20u
 /* Staged families: pipeline depth (stages in flight) in bits 12..15 (2..8;
  * 0 lets the plan choose).  A tuning knob like the stage width. */
 #define DD_CONFIG_NSTAGE_SHIFT 12u

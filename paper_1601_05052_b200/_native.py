@@ -22,6 +22,7 @@ DD_CONFIG_GPU_TILING = 0x1
 DD_CONFIG_HIGH_OCCUPANCY = 0x2
 DD_CONFIG_TIME_MAJOR = 0x8
 DD_CONFIG_PACKED_STAGES = 0x10
+DD_CONFIG_WIDE_STAGES = 0x20
 DD_CONFIG_CPS_SHIFT = 8
 DD_CONFIG_CPS_MASK = 0xF << DD_CONFIG_CPS_SHIFT
 DD_CONFIG_NSTAGE_SHIFT = 12

@@ -443,7 +443,8 @@ dd_status dd_validate_config(const dd_config* k, uint32_t num_dms, uint32_t s,
                                              std::to_string(L.max_accumulators));
   if (k->staging > DD_STAGING_RECT) return fail(DD_ERR_INVALID_ARGUMENT, "unknown staging mode");
   if (k->flags & ~(DD_CONFIG_GPU_TILING | DD_CONFIG_HIGH_OCCUPANCY | DD_CONFIG_TIME_MAJOR |
-                   DD_CONFIG_PACKED_STAGES | DD_CONFIG_CPS_MASK | DD_CONFIG_NSTAGE_MASK))
+                   DD_CONFIG_PACKED_STAGES | DD_CONFIG_CPS_MASK | DD_CONFIG_NSTAGE_MASK |
+                   DD_CONFIG_WIDE_STAGES))
     return fail(DD_ERR_INVALID_ARGUMENT, "unknown config flags");
 
   const uint32_t ns = (k->flags & DD_CONFIG_NSTAGE_MASK) >> DD_CONFIG_NSTAGE_SHIFT;
@@ -521,13 +522,14 @@ bool smem_geometry(const dd_context* c, uint32_t tile_time, uint32_t tile_dm, ui
   // DEDISP_B200_STAGE_CPS / _NSTAGE pin the shape (tuning experiments).
   uint32_t top_cps = 8;
   uint32_t ns_opts[] = {3, 2};
-  const uint32_t want_cps = (flags & DD_CONFIG_CPS_MASK) >> DD_CONFIG_CPS_SHIFT;
+  const uint32_t want_cps = ((flags & DD_CONFIG_CPS_MASK) >> DD_CONFIG_CPS_SHIFT) *
+                            ((flags & DD_CONFIG_WIDE_STAGES) ? 2u : 1u);
   const uint32_t want_ns = (flags & DD_CONFIG_NSTAGE_MASK) >> DD_CONFIG_NSTAGE_SHIFT;
   if (want_cps >= 1) top_cps = want_cps;
   if (want_ns >= 2 && want_ns <= 8) ns_opts[0] = ns_opts[1] = want_ns;
   if (const char* e = std::getenv("DEDISP_B200_STAGE_CPS")) {
     const uint32_t v = static_cast<uint32_t>(std::atoi(e));
-    if (v >= 1 && v <= 15) top_cps = v;
+    if (v >= 1 && v <= 30) top_cps = v;
   }
   if (const char* e = std::getenv("DEDISP_B200_STAGE_NSTAGE")) {
     const uint32_t v = static_cast<uint32_t>(std::atoi(e));

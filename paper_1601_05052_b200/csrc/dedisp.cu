@@ -286,6 +286,16 @@ struct ChannelUnroll<B, decltype(void(B::kUnroll))> {
   static constexpr uint32_t value = B::kUnroll;
 };
 
+// Bodies that prefetch the next channel's record entry (kGroupPrefetch).
+template <class B, class = void>
+struct GroupPrefetch {
+  static constexpr bool value = false;
+};
+template <class B>
+struct GroupPrefetch<B, decltype(void(B::kGroupPrefetch))> {
+  static constexpr bool value = B::kGroupPrefetch;
+};
+
 // Bodies that run a whole stage themselves (kStagePipe = true).
 template <class B, class = void>
 struct HasStagePipe {
@@ -351,7 +361,9 @@ __device__ __forceinline__ void staged_loop_with(const TiledArgs& a, uint8_t* sm
         const auto one = [&](uint32_t cc) {
           const uint32_t* r = reinterpret_cast<const uint32_t*>(rbase + cc * a.rec_bytes);
           const float* w = wbase + window_offset<PK>(a, ch0, cc);
-          if constexpr (Body::kRowBase)
+          if constexpr (GroupPrefetch<Body>::value)
+            body.channel(r, w, cc + 1 < ncs);
+          else if constexpr (Body::kRowBase)
             body.channel(r, w);
           else
             body.channel(r, w + ((p.t0 + r[0]) & 3u));
@@ -792,6 +804,9 @@ __device__ __forceinline__ void tmem_wait_ld() {
 #ifndef DDB_TMEM_TAIL_EARLY
 #define DDB_TMEM_TAIL_EARLY 1
 #endif
+#ifndef DDB_TMEM_GPREFETCH
+#define DDB_TMEM_GPREFETCH 0
+#endif
 // launch bound of k_tmemwin: 288 threads (up to 8 consumer warps), or an A/B
 // build bounded to 160 threads x 2 CTAs (<= 204 registers)
 #ifndef DDB_TMEM_LB2
@@ -879,7 +894,9 @@ struct TmemBody {
         n.off[k + 1] = v.y;
       }
     }
-    const uint2 g = *reinterpret_cast<const uint2*>(r + 4 + a.tile_dm + 2 * (dml / K));
+    const uint2 g = (DDB_TMEM_GPREFETCH && gvalid_)
+                        ? gnext_
+                        : *reinterpret_cast<const uint2*>(r + 4 + a.tile_dm + 2 * (dml / K));
     // fast iff the window fits the columns this variant stages
     n.nv = g.x <= static_cast<uint32_t>((32 + kTail) / 4) ? g.x : 0u;
     n.base = w + col + g.y;  // w: the channel's 16-byte aligned row (kRowBase)
@@ -1032,6 +1049,22 @@ struct TmemBody {
     Pre n;
     fetch(n, r, w);
     commit(n);
+    accumulate(n.off, n.nv != 0, n.base);
+  }
+  // DDB_TMEM_GPREFETCH: the next channel's window geometry (its record's
+  // group entry) is read before this channel's TMEM reads and adds, so the
+  // next fetch starts with its window loads
+  static constexpr bool kGroupPrefetch = DDB_TMEM_GPREFETCH != 0;
+  uint2 gnext_ = make_uint2(0u, 0u);
+  bool gvalid_ = false;
+  __device__ __forceinline__ void channel(const uint32_t* r, const float* w, bool has_next) {
+    Pre n;
+    fetch(n, r, w);
+    commit(n);
+    gvalid_ = has_next;
+    if (has_next)
+      gnext_ = *reinterpret_cast<const uint2*>(r + a.rec_bytes / 4u + 4 + a.tile_dm +
+                                               2 * (dml / K));
     accumulate(n.off, n.nv != 0, n.base);
   }
   // kStagePipe: the channels of one stage (fixed slots of win_cap floats),

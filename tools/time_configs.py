@@ -4,7 +4,8 @@
 
 Extra fields: "g" requests GPU tiling (tile_time need not divide s),
 "cpsN" pins N channels per pipeline stage, "occ" the TMEM three-CTA build,
-"nsN" N pipeline stages, "tm" time-major CTA raster, "pk" packed stages.
+"nsN" N pipeline stages, "tm" time-major CTA raster, "pk" packed stages,
+"wide" twice the cps channels per stage.
 --cold flushes L2 before every timed run (dd_plan_time_ex).
 """
 import os
@@ -44,7 +45,8 @@ def main():
                          flags=(next((int(x[2:]) for x in extra if x.startswith("ns")), 0)
                                 << N.DD_CONFIG_NSTAGE_SHIFT)
                          | (N.DD_CONFIG_TIME_MAJOR if "tm" in extra else 0)
-                         | (N.DD_CONFIG_PACKED_STAGES if "pk" in extra else 0))
+                         | (N.DD_CONFIG_PACKED_STAGES if "pk" in extra else 0)
+                         | (N.DD_CONFIG_WIDE_STAGES if "wide" in extra else 0))
         except ValueError as e:
             print(f"{spec:28s} invalid: {e}")
             continue
