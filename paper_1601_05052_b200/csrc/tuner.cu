@@ -200,6 +200,14 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
         c.flags = flags;
         v.push_back(c);
       }
+      if (num_dms <= 128) {  // where K3 competes: two stages of 24 channels
+        dd_config c = k;
+        c.dm_tile_depth = depth;
+        c.staging = DD_STAGING_SMEM;
+        c.flags = DD_CONFIG_WIDE_STAGES | (12u << DD_CONFIG_CPS_SHIFT) |
+                  (2u << DD_CONFIG_NSTAGE_SHIFT);
+        v.push_back(c);
+      }
       // packed stages where a packed build exists (the large-delay shapes)
       ddb::KernelFn packed = nullptr;
       find_smem_kernel(k.work_dm, k.work_time, nullptr, k.items_time, &packed);
