@@ -86,7 +86,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // hardware until the phase completes (or the hint expires) instead of
 // polling, so the waiting producer does not steal issue slots from the
 // consumer warps of its scheduler.
+#ifndef DDB_PRODUCER_SLEEP_NS
+#define DDB_PRODUCER_SLEEP_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  if constexpr (DDB_PRODUCER_SLEEP_NS > 0) {
+    // A/B: poll, then a plain timed sleep between polls
+    while (!mbar_try_wait(bar, parity)) __nanosleep(DDB_PRODUCER_SLEEP_NS);
+    return;
+  }
   uint32_t ok = 0;
   while (!ok) {
     asm volatile(

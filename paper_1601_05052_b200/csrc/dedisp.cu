@@ -807,6 +807,25 @@ __device__ __forceinline__ void tmem_wait_ld() {
 #ifndef DDB_TMEM_GPREFETCH
 #define DDB_TMEM_GPREFETCH 0
 #endif
+// the warp's TMEM address broadcast from lane 0 (__shfl_sync), so ptxas
+// keeps it in a uniform register: the window stores address tmem[UR + imm]
+// with no R2UR per store and the DM reads add it as a uniform operand.
+// Measured (profiles/r02_ab_tmem_uniform.txt, --cold): W = 12 K = 8 at
+// Apertif d=4096 5.994 -> 5.805 ms, d=1024 1.575 -> 1.524 ms; the W = 20
+// build (d=128) 0.262 -> 0.270 ms, so it is applied to W = 12 only
+#ifndef DDB_TMEM_UNIFORM
+#define DDB_TMEM_UNIFORM 1
+#endif
+// the x8 window tail stored unconditionally (columns no DM reads when the
+// window fits 32): no branch + WARPSYNC around the tail store
+// the channel's window geometry (vectors, start) broadcast from lane 0 too:
+// its tests become uniform branches
+#ifndef DDB_TMEM_UNIFORM_G
+#define DDB_TMEM_UNIFORM_G 0
+#endif
+#ifndef DDB_TMEM_TAIL_ALWAYS
+#define DDB_TMEM_TAIL_ALWAYS 0
+#endif
 // launch bound of k_tmemwin: 288 threads (up to 8 consumer warps), or an A/B
 // build bounded to 160 threads x 2 CTAs (<= 204 registers)
 #ifndef DDB_TMEM_LB2
@@ -854,6 +873,7 @@ struct TmemBody {
     dml = (warp / warps_time) * K;
     // lanes (warp % 4) * 32.. are this warp's TMEM rows; COLS columns per warp
     taddr = tmem_base + (((warp & 3) * 32) << 16) + (warp >> 2) * COLS * kBufs;
+    if constexpr (DDB_TMEM_UNIFORM && W == 12) taddr = __shfl_sync(0xffffffffu, taddr, 0);
   }
   __device__ __forceinline__ void zero() {
 #pragma unroll
@@ -894,9 +914,14 @@ struct TmemBody {
         n.off[k + 1] = v.y;
       }
     }
-    const uint2 g = (DDB_TMEM_GPREFETCH && gvalid_)
+    const uint2 g0 = (DDB_TMEM_GPREFETCH && gvalid_)
                         ? gnext_
                         : *reinterpret_cast<const uint2*>(r + 4 + a.tile_dm + 2 * (dml / K));
+    uint2 g = g0;
+    if constexpr (DDB_TMEM_UNIFORM_G) {
+      g.x = __shfl_sync(0xffffffffu, g.x, 0);
+      g.y = __shfl_sync(0xffffffffu, g.y, 0);
+    }
     // fast iff the window fits the columns this variant stages
     n.nv = g.x <= static_cast<uint32_t>((32 + kTail) / 4) ? g.x : 0u;
     n.base = w + col + g.y;  // w: the channel's 16-byte aligned row (kRowBase)
@@ -960,7 +985,7 @@ struct TmemBody {
       tmem_st32(taddr, n.win);
     }
     if constexpr (kTailEarly) {
-      if (n.nv > 8) tmem_st8(taddr + 32, n.tail);
+      if (DDB_TMEM_TAIL_ALWAYS || n.nv > 8) tmem_st8(taddr + 32, n.tail);
     } else if constexpr (kTail > 0) {
       // columns 32.. of the widest window (alignment + SPAN + W): an x8,
       // x16 or x32 store sized at compile time keeps the extra live
