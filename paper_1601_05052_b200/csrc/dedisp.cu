@@ -853,7 +853,10 @@ struct TmemBody {
   // reaches it (measured: 8 always 6.68 ms, 7 + 1 predicated 6.53, 6 + 2
   // 6.56 at Apertif d=4096 -- the predicated vector saves shared-memory
   // bandwidth, but each predicated register stays live across the channel)
-  static constexpr int kHeadAlways = 7;
+#ifndef DDB_TMEM_HEAD_ALWAYS
+#define DDB_TMEM_HEAD_ALWAYS 7
+#endif
+  static constexpr int kHeadAlways = DDB_TMEM_HEAD_ALWAYS;
   // window columns beyond the first 32: 0, 8, 16 or 32
   static constexpr int kNeed = W + SPAN + 3 - 32;
   static constexpr int kTail = kNeed <= 0 ? 0 : kNeed <= 8 ? 8 : kNeed <= 16 ? 16 : 32;
