@@ -1282,6 +1282,12 @@ struct RectBody {
 #ifndef DDB_RECT_PREFETCH
 #define DDB_RECT_PREFETCH 0
 #endif
+// the box misalignment handed to the consumers through shared memory (the
+// producer already has it) instead of a global load of the group low per
+// consumer thread and stage
+#ifndef DDB_RECT_MIS_SMEM
+#define DDB_RECT_MIS_SMEM 1
+#endif
 
 template <int K, int W, int IT>
 __global__ void __launch_bounds__(1024 + 32) k_rect(const __grid_constant__ CUtensorMap tmap,
@@ -1289,6 +1295,7 @@ __global__ void __launch_bounds__(1024 + 32) k_rect(const __grid_constant__ CUte
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem + 64);
+  __shared__ uint32_t mis_s[8];  // per slot: (t0 + lo_g) & 3 (nstage <= 8)
   // stage s: rect_ch x rect_w floats (128-byte aligned), then the offsets
   // (rec_bytes: a group's offsets, rect_ch x tile_dm u32 padded to 16 B)
   const uint32_t box_bytes = a.rect_ch * a.rect_w * 4u;
@@ -1326,8 +1333,9 @@ __global__ void __launch_bounds__(1024 + 32) k_rect(const __grid_constant__ CUte
       // the box starts at the 16-byte aligned sample at or below t0 + lo_g
       // (TMA tile loads fault on an unaligned row start); the consumers add
       // the misalignment back
-      const int32_t x0 =
-          static_cast<int32_t>((t0 + __ldg(a.glo + b * a.rect_groups + grp)) & ~3u);
+      const uint32_t xs = t0 + __ldg(a.glo + b * a.rect_groups + grp);
+      const int32_t x0 = static_cast<int32_t>(xs & ~3u);
+      if constexpr (DDB_RECT_MIS_SMEM) mis_s[slot] = xs & 3u;  // published by the arrive below
       uint8_t* st = stages + slot * stage_bytes;
       uint64_t* bar = &full[slot];
       mbar_expect_tx(bar, box_bytes + a.rec_bytes);
@@ -1365,8 +1373,10 @@ __global__ void __launch_bounds__(1024 + 32) k_rect(const __grid_constant__ CUte
     consumer_wait(&full[slot], (g / a.nstage) & 1u);
     const uint8_t* st = stages + slot * stage_bytes;
     const uint32_t grp0 = g_begin + q;
-    const float* rows = reinterpret_cast<const float*>(st) +
-                        ((t0 + __ldg(a.glo + (b_first + g / nchunk) * a.rect_groups + grp0)) & 3u);
+    const uint32_t mis =
+        DDB_RECT_MIS_SMEM ? mis_s[slot]
+                          : ((t0 + __ldg(a.glo + (b_first + g / nchunk) * a.rect_groups + grp0)) & 3u);
+    const float* rows = reinterpret_cast<const float*>(st) + mis;
     const uint32_t* offs = reinterpret_cast<const uint32_t*>(st + ((box_bytes + 127u) & ~127u));
     const uint32_t grp = grp0;
     // this launch's channels of the group (a channel-range pass may start or
