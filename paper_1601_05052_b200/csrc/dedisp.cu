@@ -1282,11 +1282,17 @@ struct RectBody {
 #ifndef DDB_RECT_PREFETCH
 #define DDB_RECT_PREFETCH 0
 #endif
-// the box misalignment handed to the consumers through shared memory (the
-// producer already has it) instead of a global load of the group low per
-// consumer thread and stage
+// A/B switches, both off: measured within +-1 us at d=2..16 and mixed at
+// d=64 (profiles/r02_ab_rect_lo.txt).  MIS_SMEM: the box misalignment handed
+// to the consumers through shared memory (the producer already has it)
+// instead of a global load of the group low per consumer thread and stage
 #ifndef DDB_RECT_MIS_SMEM
-#define DDB_RECT_MIS_SMEM 1
+#define DDB_RECT_MIS_SMEM 0
+#endif
+// the producer loads the next chunk's group low one chunk ahead, so the
+// global load's latency overlaps its wait for the next free slot
+#ifndef DDB_RECT_LO_AHEAD
+#define DDB_RECT_LO_AHEAD 0
 #endif
 
 template <int K, int W, int IT>
@@ -1326,14 +1332,26 @@ __global__ void __launch_bounds__(1024 + 32) k_rect(const __grid_constant__ CUte
   __syncthreads();
   if (threadIdx.x >= consumers * 32) {  // producer warp: lane 0 issues
     if ((threadIdx.x & 31) != 0) return;
+    const auto group_lo = [&](uint32_t g) {
+      return __ldg(a.glo + (b_first + g / nchunk) * a.rect_groups + g_begin + g % nchunk);
+    };
+    uint32_t lo_next = (DDB_RECT_LO_AHEAD && total > 0) ? group_lo(0) : 0u;
     for (uint32_t g = 0; g < total; ++g) {
       const uint32_t slot = g % a.nstage, use = g / a.nstage;
+      uint32_t lo;
+      if constexpr (DDB_RECT_LO_AHEAD) {
+        lo = lo_next;
+        if (g + 1 < total) lo_next = group_lo(g + 1);
+      } else {
+        lo = 0u;
+      }
       if (use > 0) mbar_wait_sleep(&empty[slot], (use - 1) & 1u);
       const uint32_t b = b_first + g / nchunk, grp = g_begin + g % nchunk;
+      if constexpr (!DDB_RECT_LO_AHEAD) lo = __ldg(a.glo + b * a.rect_groups + grp);
       // the box starts at the 16-byte aligned sample at or below t0 + lo_g
       // (TMA tile loads fault on an unaligned row start); the consumers add
       // the misalignment back
-      const uint32_t xs = t0 + __ldg(a.glo + b * a.rect_groups + grp);
+      const uint32_t xs = t0 + lo;
       const int32_t x0 = static_cast<int32_t>(xs & ~3u);
       if constexpr (DDB_RECT_MIS_SMEM) mis_s[slot] = xs & 3u;  // published by the arrive below
       uint8_t* st = stages + slot * stage_bytes;

@@ -53,7 +53,7 @@ def main():
         runs = p.time(x.data_ptr(), out.data_ptr(), warmup=2, repeats=10, flush_l2=cold)
         ms = sorted(runs)[len(runs) // 2] * 1e3
         i = p.info()
-        print(f"{spec:28s} {i['family']:7s} {ms:8.3f} ms  {flop / ms / 1e6:9.1f} GFLOP/s  "
+        print(f"{spec:28s} {i['family']:7s} {ms:8.4f} ms  {flop / ms / 1e6:9.1f} GFLOP/s  "
               f"smem={i['smem_bytes']} stages={i['stages']}x{i['channels_per_stage']} "
               f"regs={i['registers']} ctas/sm={i['ctas_per_sm']}", flush=True)
 
