@@ -282,11 +282,18 @@ dd_status dd_enumerate_gpu_configs(dd_context* ctx, const dd_setup* setup, uint3
             if (block < 32 || block > 512 || num_dms % (idm * wd) != 0) continue;
             if (find_rect_kernel(wd, wt, it) == nullptr) continue;
             // 32, 64 or 128 channels per TMA box (4 stages): wider boxes
-            // amortise the per-box cost (measured, small d)
+            // amortise the per-box cost (measured, small d); the wide boxes
+            // also with 2 stages, which leaves room for more CTAs per SM
+            // (Apertif d=2: 128 channels x 2 stages 25.6 us vs x 4 35.7 us,
+            // profiles/r02_rect_d2_stage_sweep.txt)
             for (uint32_t cps : {2u, 4u, 8u}) {
               dd_config c{it, idm, wt, wd, 1, DD_STAGING_RECT,
                           DD_CONFIG_GPU_TILING | (cps << DD_CONFIG_CPS_SHIFT)};
               v.push_back(c);
+              if (cps >= 4) {
+                c.flags |= 2u << DD_CONFIG_NSTAGE_SHIFT;
+                v.push_back(c);
+              }
             }
           }
   }
