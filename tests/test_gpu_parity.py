@@ -656,7 +656,10 @@ def test_every_gpu_space_config_is_bit_exact(dev, golden, name, d):
         try:  # the tuner skips what the plan rejects for this table (dd_tune)
             p = dev.plan(sh.data_ptr(), c, d, s, t, t, cfg, depth, staging, flags=flags)
         except ValueError:
-            rejected += 1
+            # K6 rectangles are enumerated for every d <= 128 and rejected by
+            # the plan when a group's delay span exceeds the 256-sample TMA
+            # box (all of LOFAR's): not counted against the space
+            rejected += staging != "rect"
             continue
         families.add(p.info()["family"])
         p.execute(x.data_ptr(), out.data_ptr())
