@@ -14,3 +14,5 @@ for lib in default pipe; do
 done
 done > $O/ab.txt 2>&1
 grep -E "^==|^--|ms " $O/ab.txt | awk '/^==|^--/{print; next}{print "   ",$1,$3,$4,$7,$8,$9}'
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "every_gpu_space" > $O/space_test.log 2>&1
+tail -3 $O/space_test.log
