@@ -1301,10 +1301,12 @@ dd_status upload_staged(dd_context* c, float* d_dst, uint64_t pitch, const float
 
 // Device buffer -> pageable host buffer (contiguous), chunked through the
 // bounce buffers: the DMA of chunk k+1 runs while host threads copy chunk k.
-dd_status download_staged(dd_context* c, void* h_dst, const void* d_src, uint64_t bytes) {
+dd_status download_staged(dd_context* c, void* h_dst, const void* d_src, uint64_t bytes,
+                          cudaStream_t stream = nullptr) {
+  if (stream == nullptr) stream = c->stream;
   if (bytes < kBounceMin) {
-    DD_TRY(dd_copy_d2h(c, h_dst, d_src, bytes));
-    DD_CUDA(cudaStreamSynchronize(c->stream));
+    DD_CUDA(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, stream));
+    DD_CUDA(cudaStreamSynchronize(stream));
     return DD_OK;
   }
   DD_TRY(bounce_ready(c));
@@ -1312,8 +1314,8 @@ dd_status download_staged(dd_context* c, void* h_dst, const void* d_src, uint64_
   auto issue = [&](uint64_t k) -> dd_status {
     const uint64_t lo = k * kBounce, nb = std::min(kBounce, bytes - lo);
     DD_CUDA(cudaMemcpyAsync(c->h_bounce[k & 1], static_cast<const char*>(d_src) + lo, nb,
-                            cudaMemcpyDeviceToHost, c->stream));
-    DD_CUDA(cudaEventRecord(c->ev_bounce[k & 1], c->stream));
+                            cudaMemcpyDeviceToHost, stream));
+    DD_CUDA(cudaEventRecord(c->ev_bounce[k & 1], stream));
     return DD_OK;
   };
   DD_TRY(issue(0));
@@ -1474,8 +1476,38 @@ dd_status dd_dedisperse(dd_context* c, const float* h_in, uint32_t channels, uin
   if (num_dms == 0) return fail(DD_ERR_INVALID_ARGUMENT, "delay table holds no trials");
   if (channels == 0 || s == 0) return fail(DD_ERR_INVALID_ARGUMENT, "empty setup");
   const uint64_t entries = static_cast<uint64_t>(num_dms) * channels;
+  // the table is compared with the cached copy first (a survey or a tuner
+  // calls with the same table) and its max delay reused; large tables are
+  // compared / scanned by the host pool
+  if (entries >= (1ull << 20)) DD_TRY(bounce_ready(c));
+  const unsigned parts = entries >= (1ull << 20) ? c->pool->size() : 1u;
+  const uint64_t per = (entries + parts - 1) / parts;
+  const bool same_table = [&] {
+    if (c->cached_table.size() != entries) return false;
+    std::vector<char> eq(parts, 1);
+    auto cmp = [&](unsigned i) {
+      const uint64_t lo = std::min(entries, per * i), hi = std::min(entries, lo + per);
+      eq[i] = std::memcmp(c->cached_table.data() + lo, h_shifts + lo, (hi - lo) * 4) == 0;
+    };
+    if (parts > 1) c->pool->run(parts, cmp);
+    else cmp(0);
+    return std::all_of(eq.begin(), eq.end(), [](char e) { return e != 0; });
+  }();
   uint32_t md = 0;
-  for (uint64_t i = 0; i < entries; ++i) md = std::max(md, h_shifts[i]);
+  if (same_table) {
+    md = c->cached_max_delay;
+  } else {
+    std::vector<uint32_t> mx(parts, 0);
+    auto scan = [&](unsigned i) {
+      const uint64_t lo = std::min(entries, per * i), hi = std::min(entries, lo + per);
+      uint32_t m = 0;
+      for (uint64_t j = lo; j < hi; ++j) m = std::max(m, h_shifts[j]);
+      mx[i] = m;
+    };
+    if (parts > 1) c->pool->run(parts, scan);
+    else scan(0);
+    md = *std::max_element(mx.begin(), mx.end());
+  }
   const uint64_t needed = static_cast<uint64_t>(s) + md;
   if (num_samples < needed)
     return fail(DD_ERR_INVALID_ARGUMENT, "filterbank too short: need " + std::to_string(needed) +
@@ -1513,9 +1545,7 @@ dd_status dd_dedisperse(dd_context* c, const float* h_in, uint32_t channels, uin
                                           limits->max_accumulators) << 8
                                        : 0)};
   const bool same = c->cached_plan != nullptr && old_sh == c->d_sh &&
-                    std::memcmp(key, c->cached_key, sizeof(key)) == 0 &&
-                    c->cached_table.size() == entries &&
-                    std::memcmp(c->cached_table.data(), h_shifts, sh_bytes) == 0;
+                    std::memcmp(key, c->cached_key, sizeof(key)) == 0 && same_table;
   if (!same) {
     dd_plan_destroy(c->cached_plan);
     c->cached_plan = nullptr;
@@ -1525,6 +1555,7 @@ dd_status dd_dedisperse(dd_context* c, const float* h_in, uint32_t channels, uin
     DD_TRY(plan_one_shot(c, static_cast<uint32_t*>(c->d_sh), channels, num_dms, s, num_samples,
                          pitch, k, limits, &c->cached_plan, &ran));
     c->cached_table.assign(h_shifts, h_shifts + entries);
+    c->cached_max_delay = md;
     std::memcpy(c->cached_key, key, sizeof(key));
     c->last_run = ran;
     c->last_family = c->cached_plan->family;

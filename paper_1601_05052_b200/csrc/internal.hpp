@@ -67,6 +67,7 @@ struct dd_context {
   uint64_t bounce_bytes = 0;
   cudaEvent_t ev_bounce[2] = {nullptr, nullptr};
   ddb::HostPool* pool = nullptr;
+  uint32_t cached_max_delay = 0;  // of cached_table
 };
 
 #include <cuda.h>
