@@ -20,6 +20,21 @@ def spec(r):
                               b["dm_tile_depth"], b["staging"]] + x))
 
 
+def flags_of_spec(spec_str):
+    """The dd_config flags tools/time_configs.py builds from a spec (the
+    inverse of spec() above; "cpsN" and "occ" map to the same bits the plan's
+    stage_channels / high_occupancy arguments set)."""
+    extra = spec_str.split(",")[6:]
+    f = 1 if "g" in extra else 0
+    f |= 2 if "occ" in extra else 0
+    f |= 8 if "tm" in extra else 0
+    f |= 0x10 if "pk" in extra else 0
+    f |= 0x20 if "wide" in extra else 0
+    f |= next((int(x[3:]) for x in extra if x.startswith("cps")), 0) << 8
+    f |= next((int(x[2:]) for x in extra if x.startswith("ns")), 0) << 12
+    return f
+
+
 if __name__ == "__main__":
     d = json.load(open(sys.argv[1]))
     recs = sorted((r for r in d["records"] if r["mean_time_s"] > 0), key=lambda r: r["mean_time_s"])
